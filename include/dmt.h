@@ -1,0 +1,245 @@
+/*
+ * dmt.h -- C ABI of libdmt.so, the sm_100a kernels of the DMT / SPTT hot path
+ * (arXiv 2403.00877).  Plain pointers, sizes and a cudaStream_t; no torch
+ * types.  Every entry point is stream-ordered, never allocates device memory
+ * and never synchronises the host; callers own all buffers (workspace sizes
+ * are queried with the *_workspace_size functions).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/towersim):
+ *   dmt_lengths_to_offsets   -- offsets of SparseBatch bags           embedding.py:215-226
+ *   dmt_kjt_bucketize        -- step a bundling per shard owner       exchange.py:162-178
+ *   dmt_pooled_lookup_fwd    -- lookup / _shard_lookup (+ fused step-c
+ *                               permute and step-d stacking)          embedding.py:64-85,
+ *                                                                      exchange.py:130-146,324-365
+ *   dmt_assemble             -- _combine_pieces, step-e regroup,
+ *                               step-f concat, realign                exchange.py:112-127,397-437,
+ *                                                                      448-449,465-486
+ *   dmt_batched_copy         -- in-process all_to_all delivery         simnet.py:117-146
+ *   dmt_pooled_lookup_bwd    -- (absent in the reference: backward of
+ *                               lookup with fused SGD / row-wise Adagrad)
+ *   dmt_gemm                 -- tm_dlrm_forward / crossnet_layer /
+ *                               tm_dcn_forward matmuls + epilogues    towermod.py:110-158
+ *
+ * Status codes map onto the reference exception classes (errors.py):
+ */
+#ifndef DMT_H_
+#define DMT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dmt_stream_t; /* == cudaStream_t */
+
+enum dmt_status {
+  DMT_OK = 0,
+  DMT_ERR_DOMAIN = -1,      /* DomainError        errors.py:11  */
+  DMT_ERR_SHAPE = -2,       /* ShapeError         errors.py:23  */
+  DMT_ERR_PLAN = -3,        /* PlanError          errors.py:27  */
+  DMT_ERR_LOOKUP = -4,      /* TableLookupError   errors.py:35  */
+  DMT_ERR_PROTOCOL = -5,    /* ProtocolError      errors.py:19  */
+  DMT_ERR_UNSUPPORTED = -6, /* DomainError (unsupported dtype / shape) */
+  DMT_ERR_CUDA = -10        /* CUDA launch / runtime failure */
+};
+
+enum dmt_dtype { DMT_F32 = 0, DMT_BF16 = 1, DMT_F64 = 2, DMT_F16 = 3 };
+
+enum dmt_pooling { DMT_POOL_NONE = 0, DMT_POOL_SUM = 1, DMT_POOL_MEAN = 2 };
+
+/* device-side error flag bits (dmt_pooled_lookup_* `err`) */
+enum dmt_err_bits { DMT_EBIT_INDEX = 1, DMT_EBIT_BAGLEN = 2 };
+
+/* ---------------------------------------------------------------- KJT ---- */
+
+/* offsets[0] = 0, offsets[i+1] = offsets[i] + lengths[i]  (n lengths).
+ * `scratch` must hold dmt_lengths_to_offsets_workspace_size(n) bytes. */
+size_t dmt_lengths_to_offsets_workspace_size(int64_t n);
+int dmt_lengths_to_offsets(const int32_t* lengths, int64_t n, int64_t* offsets,
+                           void* scratch, dmt_stream_t stream);
+
+/* Step a bundling.  Input: one rank's KJT, keys (features) major:
+ * lengths[F*B], offsets[F*B+1], values[offsets[F*B]].
+ * slot_feature[num_slots]: feature position shipped by each send slot (slots
+ * ordered owner-major, shard-id order inside an owner -- exchange.py:172-178).
+ * slot_value_offset[num_slots+1]: where each slot's values start in
+ * out_values (exclusive prefix of the slots' nnz; all device arrays).
+ * Output: out_lengths[num_slots*B], out_values. */
+int dmt_kjt_bucketize(const int32_t* lengths, const int64_t* offsets, const int32_t* values,
+                      int32_t B, int32_t num_slots, const int32_t* slot_feature,
+                      const int64_t* slot_value_offset, int32_t* out_lengths,
+                      int32_t* out_values, dmt_stream_t stream);
+
+/* Device-side slot offsets (when per-feature nnz is not known on the host):
+ * slot_value_offset[s+1] - slot_value_offset[s] = nnz(slot_feature[s]). */
+int dmt_kjt_slot_offsets(const int64_t* offsets, int32_t B, int32_t num_slots,
+                         const int32_t* slot_feature, int64_t* slot_value_offset,
+                         dmt_stream_t stream);
+
+/* ------------------------------------------------------- pooled lookup ---- */
+
+/* One segment = `nbags` consecutive bags of one table shard whose pooled rows
+ * go to out + b*out_ld (b = 0..nbags-1).  Bag i of the segment is global bag
+ * bag_begin + i of the (offsets, indices) arrays.  Indices are table-global;
+ * rows outside [row_begin, row_begin+rows) are skipped when `row_filter` (row-
+ * wise shards, exchange.py:138-144) and flagged DMT_EBIT_INDEX otherwise. */
+typedef struct dmt_lookup_segment {
+  const void* weights; /* shard rows, row-major, row r at weights + (r-row_begin)*ld */
+  void* out;           /* fwd: pooled output; bwd: gradient of the pooled output */
+  void* state;         /* bwd row-wise Adagrad accumulator (float per row) or NULL */
+  int64_t ld;          /* weights row stride (elements) */
+  int64_t out_ld;      /* out row stride (elements) */
+  int64_t bag_begin;   /* first global bag */
+  int64_t row_begin;   /* first table row held by the shard */
+  int64_t key_base;    /* bwd: base of this shard's rows in the sort key space */
+  int32_t rows;        /* rows held by the shard */
+  int32_t width;       /* columns of the shard */
+  int32_t nbags;       /* bags in this segment */
+  int32_t pooling;     /* dmt_pooling */
+  int32_t row_filter;  /* 1 = row-wise shard: filter + rebase */
+  int32_t pad_;
+} dmt_lookup_segment;
+
+/* Forward.  All segments share dtype.  Accumulation is fp32 (f32/bf16/f16) or
+ * fp64 (f64) in bag order -- bit-exact against the reference's sequential sum.
+ * err (device int32, may be NULL) receives dmt_err_bits.  segs is the device
+ * copy of the segment table, segs_host the identical host copy (used only for
+ * launch shaping: widths, alignment, bag counts). */
+int dmt_pooled_lookup_fwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host,
+                          int32_t num_segs, const int64_t* offsets, const int32_t* indices,
+                          int32_t dtype, int32_t* err, dmt_stream_t stream);
+
+/* Backward with fused optimizer (absent in the reference).
+ * segs[i].out is the gradient of the pooled rows, segs[i].weights is updated
+ * in place (const is cast away), key_base/rows define a disjoint key range per
+ * shard (segments of the same shard share it).  Duplicate rows are reduced
+ * after a stable radix sort, so the update is deterministic.
+ * optimizer: 0 = SGD (w -= lr*g), 1 = row-wise Adagrad
+ * (s += mean(g^2); w -= lr*g/(sqrt(s)+eps)). */
+enum dmt_optimizer { DMT_OPT_SGD = 0, DMT_OPT_ROWWISE_ADAGRAD = 1 };
+size_t dmt_pooled_lookup_bwd_workspace_size(int64_t nnz, int64_t key_space, int32_t num_segs);
+int dmt_pooled_lookup_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host,
+                          int32_t num_segs, const int64_t* offsets, const int32_t* indices,
+                          int64_t nnz, int64_t key_space, int32_t dtype, int32_t optimizer,
+                          float lr, float eps, void* workspace, size_t workspace_bytes,
+                          dmt_stream_t stream);
+
+/* ------------------------------------------------------------ assemble ---- */
+
+/* dst[r, col0 + j] = sum_{s < nsrc} src_s[r*ld_s + j]   for r < rows, j < width.
+ * Sums run in source order in fp64 (f32/f64/bf16) and round once: column
+ * shards (nsrc = 1) are copies, row-wise partials (nsrc > 1) are summed in
+ * row-range order like exchange.py:118-123. */
+typedef struct dmt_assemble_block {
+  int64_t dst_col;
+  int32_t width;
+  int32_t nsrc;
+  int32_t first_src; /* index into the src table */
+  int32_t pad_;
+} dmt_assemble_block;
+
+typedef struct dmt_src {
+  const void* ptr;
+  int64_t ld;
+} dmt_src;
+
+int dmt_assemble(const dmt_assemble_block* blocks, int32_t num_blocks, int32_t max_width,
+                 const dmt_src* srcs, int64_t rows, void* dst, int64_t dst_ld, int32_t dtype,
+                 dmt_stream_t stream);
+
+/* n byte copies in one launch (in-process collective delivery). */
+typedef struct dmt_copy {
+  const void* src;
+  void* dst;
+  int64_t bytes;
+} dmt_copy;
+int dmt_batched_copy(const dmt_copy* copies, int32_t n, int64_t max_bytes, dmt_stream_t stream);
+
+/* Batched 2-D strided copies: rows x width elements of elem_bytes each,
+ * dst[r*dst_ld + j] = src[r*src_ld + j] (pack/unpack of exchange blocks in the
+ * backward: f^-1 and d^-1 send buffers). */
+typedef struct dmt_copy2d {
+  const void* src;
+  void* dst;
+  int64_t src_ld;
+  int64_t dst_ld;
+  int64_t rows;
+  int64_t width;
+} dmt_copy2d;
+int dmt_batched_copy2d(const dmt_copy2d* copies, int32_t n, int32_t elem_bytes, int64_t max_elems,
+                       dmt_stream_t stream);
+
+/* ---------------------------------------------------------------- GEMM ---- */
+
+/* D[m, n] = epilogue( sum_k A[m, k] * B[n, k] )   (both operands K-major)
+ *   bf16 / f16 operands: tcgen05.mma kind::f16, fp32 accumulate in TMEM
+ *   f32 operands:        tcgen05.mma kind::tf32, 3xTF32 split (fp32 accuracy)
+ * Epilogues (fp32 math on the TMEM accumulator):
+ *   DMT_EPI_BIAS : v = acc + bias[n]
+ *   DMT_EPI_CROSS: v = x0[m, n] * (acc + bias[n]) + xl[m, n]   (crossnet_layer,
+ *                  towermod.py:132-139); optionally u = acc + bias stored to aux
+ *   DMT_EPI_ACC  : v = acc + beta*C[m, n] (C = d)
+ * Output row m goes to d + (m / rows_per_group)*ld_group + (m % rows_per_group)*ld_d,
+ * so the per-feature DLRM projection can write straight into the tower output. */
+enum dmt_epilogue { DMT_EPI_NONE = 0, DMT_EPI_BIAS = 1, DMT_EPI_CROSS = 2, DMT_EPI_ACC = 3 };
+
+typedef struct dmt_gemm_args {
+  const void* a;   /* [m, k] row stride lda */
+  const void* b;   /* [n, k] row stride ldb */
+  void* d;         /* output */
+  const float* bias;
+  const void* x0;  /* CROSS: [m, n] row stride ld_x */
+  const void* xl;
+  void* aux;       /* CROSS: u = acc + bias, row stride ld_x (may be NULL) */
+  int64_t m, n, k;
+  int64_t lda, ldb, ld_d, ld_x;
+  int64_t rows_per_group, ld_group;
+  float beta;
+  int32_t in_dtype;  /* dmt_dtype of a, b (and x0/xl/aux for CROSS) */
+  int32_t out_dtype; /* dmt_dtype of d */
+  int32_t epilogue;
+  int32_t pad_;
+} dmt_gemm_args;
+
+int dmt_gemm(const dmt_gemm_args* args, dmt_stream_t stream);
+
+/* fp32 operands: `args->a` / `args->b` hold the tf32 "hi" parts and a_lo /
+ * b_lo the residuals (see dmt_split_tf32); bf16/f16 ignore a_lo / b_lo. */
+int dmt_gemm_ex(const dmt_gemm_args* args, const void* a_lo, const void* b_lo,
+                dmt_stream_t stream);
+
+/* hi = x with the 13 low mantissa bits cleared (exact tf32), lo = x - hi. */
+int dmt_split_tf32(const float* x, float* hi, float* lo, int64_t n, dmt_stream_t stream);
+
+/* out[j, i] = in[i, j]  (rows x cols, row strides ld_in / ld_out) */
+int dmt_transpose(const void* in, int64_t rows, int64_t cols, int64_t ld_in, void* out,
+                  int64_t ld_out, int32_t dtype, dmt_stream_t stream);
+
+/* out[c] = sum_r in[r, c] (fp32 out, fp64 accumulation, deterministic). */
+size_t dmt_column_sum_workspace_size(int64_t rows, int64_t cols);
+int dmt_column_sum(const void* in, int64_t rows, int64_t cols, int64_t ld, float* out,
+                   int32_t dtype, void* workspace, size_t workspace_bytes, dmt_stream_t stream);
+
+/* Element-wise helpers of the DCN backward:
+ *   gu = g * x0 ; dx0 += g * u         (dmt_cross_bwd_pointwise)
+ * all [rows, cols] contiguous; gu/g in in_dtype, dx0 fp32. */
+int dmt_cross_bwd_pointwise(const void* g, const void* x0, const void* u, void* gu, float* dx0,
+                            int64_t n, int32_t dtype, dmt_stream_t stream);
+
+/* w -= lr * g  (w in dtype, g fp32), n elements */
+int dmt_sgd_dense(void* w, const float* g, int64_t n, float lr, int32_t dtype,
+                  dmt_stream_t stream);
+
+/* dst (dtype_out) = src (dtype_in), n elements */
+int dmt_convert(const void* src, int32_t dtype_in, void* dst, int32_t dtype_out, int64_t n,
+                dmt_stream_t stream);
+
+/* Library identification: returns a static string ("libdmt <version> sm_100a"). */
+const char* dmt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DMT_H_ */

@@ -1,0 +1,149 @@
+"""ctypes binding of libdmt.so (the C ABI declared in include/dmt.h).
+
+There is no CPU fallback: every op in this package goes through these entry
+points and raises if the library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from .errors import STATUS_ERRORS, TowersimError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdmt.so")
+
+DT_F32, DT_BF16, DT_F64, DT_F16 = 0, 1, 2, 3
+POOL_NONE, POOL_SUM, POOL_MEAN = 0, 1, 2
+EPI_NONE, EPI_BIAS, EPI_CROSS, EPI_ACC = 0, 1, 2, 3
+OPT_SGD, OPT_ROWWISE_ADAGRAD = 0, 1
+EBIT_INDEX, EBIT_BAGLEN = 1, 2
+
+TORCH_DT = {torch.float32: DT_F32, torch.bfloat16: DT_BF16, torch.float64: DT_F64, torch.float16: DT_F16}
+POOL_CODE = {"none": POOL_NONE, "sum": POOL_SUM, "mean": POOL_MEAN}
+
+vp, i32, i64, f32, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_size_t
+
+
+class LookupSegment(C.Structure):
+    _fields_ = [
+        ("weights", vp), ("out", vp), ("state", vp),
+        ("ld", i64), ("out_ld", i64), ("bag_begin", i64), ("row_begin", i64), ("key_base", i64),
+        ("rows", i32), ("width", i32), ("nbags", i32), ("pooling", i32), ("row_filter", i32), ("pad_", i32),
+    ]
+
+
+class AssembleBlock(C.Structure):
+    _fields_ = [("dst_col", i64), ("width", i32), ("nsrc", i32), ("first_src", i32), ("pad_", i32)]
+
+
+class Src(C.Structure):
+    _fields_ = [("ptr", vp), ("ld", i64)]
+
+
+class Copy(C.Structure):
+    _fields_ = [("src", vp), ("dst", vp), ("bytes", i64)]
+
+
+class Copy2D(C.Structure):
+    _fields_ = [("src", vp), ("dst", vp), ("src_ld", i64), ("dst_ld", i64), ("rows", i64), ("width", i64)]
+
+
+class GemmArgs(C.Structure):
+    _fields_ = [
+        ("a", vp), ("b", vp), ("d", vp), ("bias", vp), ("x0", vp), ("xl", vp), ("aux", vp),
+        ("m", i64), ("n", i64), ("k", i64),
+        ("lda", i64), ("ldb", i64), ("ld_d", i64), ("ld_x", i64),
+        ("rows_per_group", i64), ("ld_group", i64),
+        ("beta", f32), ("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("pad_", i32),
+    ]
+
+
+_SIGS = {
+    "dmt_version": (C.c_char_p, []),
+    "dmt_lengths_to_offsets_workspace_size": (sz, [i64]),
+    "dmt_lengths_to_offsets": (C.c_int, [vp, i64, vp, vp, vp]),
+    "dmt_kjt_bucketize": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]),
+    "dmt_kjt_slot_offsets": (C.c_int, [vp, i32, i32, vp, vp, vp]),
+    "dmt_pooled_lookup_fwd": (C.c_int, [vp, vp, i32, vp, vp, i32, vp, vp]),
+    "dmt_pooled_lookup_bwd_workspace_size": (sz, [i64, i64, i32]),
+    "dmt_pooled_lookup_bwd": (C.c_int, [vp, vp, i32, vp, vp, i64, i64, i32, i32, f32, f32, vp, sz, vp]),
+    "dmt_assemble": (C.c_int, [vp, i32, i32, vp, i64, vp, i64, i32, vp]),
+    "dmt_batched_copy": (C.c_int, [vp, i32, i64, vp]),
+    "dmt_batched_copy2d": (C.c_int, [vp, i32, i32, i64, vp]),
+    "dmt_gemm": (C.c_int, [vp, vp]),
+    "dmt_gemm_ex": (C.c_int, [vp, vp, vp, vp]),
+    "dmt_split_tf32": (C.c_int, [vp, vp, vp, i64, vp]),
+    "dmt_transpose": (C.c_int, [vp, i64, i64, i64, vp, i64, i32, vp]),
+    "dmt_column_sum_workspace_size": (sz, [i64, i64]),
+    "dmt_column_sum": (C.c_int, [vp, i64, i64, i64, vp, i32, vp, sz, vp]),
+    "dmt_cross_bwd_pointwise": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, vp]),
+    "dmt_sgd_dense": (C.c_int, [vp, vp, i64, f32, i32, vp]),
+    "dmt_convert": (C.c_int, [vp, i32, vp, i32, i64, vp]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load_library(require_cuda: bool = True):
+    """Load libdmt.so once.  Raises (never falls back) if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise TowersimError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2403_00877_b200.build` "
+                "(there is no CPU fallback)"
+            )
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    if require_cuda and not torch.cuda.is_available():
+        raise TowersimError("libdmt needs a CUDA (sm_100a) device; none is visible (no CPU fallback)")
+    return _lib
+
+
+def lib():
+    return load_library(True)
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        cls = STATUS_ERRORS.get(status, TowersimError)
+        raise cls(f"{what} failed with libdmt status {status}")
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def struct_array(ctype, items):
+    arr = (ctype * max(1, len(items)))()
+    for i, it in enumerate(items):
+        arr[i] = it
+    return arr
+
+
+def upload_structs(arr, n: int, device) -> torch.Tensor:
+    """Copy a ctypes struct array to a device byte tensor (pinned staging)."""
+    nbytes = C.sizeof(arr) if n else 0
+    host = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+    if nbytes:
+        C.memmove(host.data_ptr(), C.addressof(arr), nbytes)
+    dev = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+    dev.copy_(host, non_blocking=True)
+    return dev

@@ -1,0 +1,325 @@
+// Data movement kernels of the exchange plus small
+// dense helpers used by the tower-module backward.
+//
+// dmt_assemble is the single gather kernel behind
+//   * _combine_pieces  (towersim/exchange.py:112-127): column shards land side
+//     by side, row-wise partials are summed in row-range order (fp64, once
+//     rounded -- matches the reference's float64 `total += mat`);
+//   * step-e regroup   (exchange.py:417-437): (feature, dest) -> (dest, feature);
+//   * step-f concat    (exchange.py:448-449) and realign (exchange.py:465-486).
+// Blocks are described by (dst column, width, source list); one CTA row-tile
+// covers all blocks of a few rows so the destination row is written
+// contiguously.
+#include "common.cuh"
+
+namespace dmt {
+
+constexpr int kAsmThreads = 256;
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kAsmThreads)
+assemble_kernel(const dmt_assemble_block* __restrict__ blocks, const dmt_src* __restrict__ srcs, int64_t rows,
+                T* __restrict__ dst, int64_t dst_ld) {
+  const dmt_assemble_block blk = blocks[blockIdx.y];
+  const int nvec = blk.width / VEC;
+  // grid.x covers rows x vectors of this block
+  const int64_t total = rows * (int64_t)nvec;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / nvec;
+    const int c = (int)(i - r * nvec) * VEC;
+    T* o = dst + r * dst_ld + blk.dst_col + c;
+    if (blk.nsrc == 1) {
+      const dmt_src s0 = srcs[blk.first_src];
+      const T* p = reinterpret_cast<const T*>(s0.ptr) + r * s0.ld + c;
+      if constexpr (VEC == 1) {
+        *o = *p;
+      } else {
+        using V = typename std::conditional<sizeof(T) * VEC == 16, uint4,
+                  typename std::conditional<sizeof(T) * VEC == 8, uint2, uint32_t>::type>::type;
+        *reinterpret_cast<V*>(o) = *reinterpret_cast<const V*>(p);
+      }
+    } else {
+      double acc[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] = 0.0;
+      for (int s = 0; s < blk.nsrc; ++s) {
+        const dmt_src sx = srcs[blk.first_src + s];
+        const T* p = reinterpret_cast<const T*>(sx.ptr) + r * sx.ld + c;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[e] += to_d<T>(p[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) o[e] = from_d<T>(acc[e]);
+    }
+  }
+}
+
+template <typename T>
+int launch_assemble(const dmt_assemble_block* blocks, int32_t nb, int32_t max_width, const dmt_src* srcs,
+                    int64_t rows, void* dst, int64_t dst_ld, cudaStream_t s, bool vec_ok) {
+  if (rows == 0 || nb == 0 || max_width == 0) return DMT_OK;
+  if (nb > 65535) return DMT_ERR_UNSUPPORTED;
+  constexpr int VEC = 16 / sizeof(T);
+  int64_t work = rows * (int64_t)max_width;
+  if (vec_ok) work /= VEC;
+  unsigned gx = (unsigned)std::min<int64_t>(ceil_div(work, kAsmThreads), 4096);
+  dim3 grid(gx, nb);
+  if (vec_ok)
+    assemble_kernel<T, VEC><<<grid, kAsmThreads, 0, s>>>(blocks, srcs, rows, (T*)dst, dst_ld);
+  else
+    assemble_kernel<T, 1><<<grid, kAsmThreads, 0, s>>>(blocks, srcs, rows, (T*)dst, dst_ld);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+// ---------------------------------------------------------------- copies ----
+__global__ void batched_copy_kernel(const dmt_copy* __restrict__ copies) {
+  const dmt_copy c = copies[blockIdx.y];
+  const int64_t n16 = ((((uintptr_t)c.src | (uintptr_t)c.dst) & 15) == 0) ? c.bytes / 16 : 0;
+  const uint4* s4 = reinterpret_cast<const uint4*>(c.src);
+  uint4* d4 = reinterpret_cast<uint4*>(c.dst);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) d4[i] = s4[i];
+  const char* s1 = reinterpret_cast<const char*>(c.src);
+  char* d1 = reinterpret_cast<char*>(c.dst);
+  for (int64_t i = n16 * 16 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.bytes; i += stride)
+    d1[i] = s1[i];
+}
+
+template <typename E>
+__global__ void batched_copy2d_kernel(const dmt_copy2d* __restrict__ copies) {
+  const dmt_copy2d c = copies[blockIdx.y];
+  const int64_t total = c.rows * c.width;
+  const E* s = reinterpret_cast<const E*>(c.src);
+  E* d = reinterpret_cast<E*>(c.dst);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / c.width, j = i - r * c.width;
+    d[r * c.dst_ld + j] = s[r * c.src_ld + j];
+  }
+}
+
+// ------------------------------------------------------------ transpose ----
+template <typename T>
+__global__ void transpose_kernel(const T* __restrict__ in, int64_t rows, int64_t cols, int64_t ld_in,
+                                 T* __restrict__ out, int64_t ld_out) {
+  __shared__ T tile[32][33];
+  int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * ld_in + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * ld_out + r] = tile[threadIdx.x][i];
+  }
+}
+
+// --------------------------------------------------------- column sum ----
+// one thread per column, rows split over grid.y; partials combined in a fixed
+// order by a second pass (deterministic).
+template <typename T>
+__global__ void colsum_partial(const T* __restrict__ in, int64_t rows, int64_t cols, int64_t ld,
+                               int64_t rows_per, double* __restrict__ part) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  int64_t r0 = (int64_t)blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
+  double acc = 0.0;
+  for (int64_t r = r0; r < r1; ++r) acc += to_d<T>(in[r * ld + c]);
+  part[(int64_t)blockIdx.y * cols + c] = acc;
+}
+
+__global__ void colsum_final(const double* __restrict__ part, int64_t cols, int nparts, float* __restrict__ out) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  double acc = 0.0;
+  for (int p = 0; p < nparts; ++p) acc += part[(int64_t)p * cols + c];
+  out[c] = (float)acc;
+}
+
+template <typename T>
+__global__ void cross_bwd_pointwise_kernel(const T* __restrict__ g, const T* __restrict__ x0,
+                                           const T* __restrict__ u, T* __restrict__ gu, float* __restrict__ dx0,
+                                           int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float gv = to_f<T>(g[i]);
+    gu[i] = from_f<T>(gv * to_f<T>(x0[i]));
+    dx0[i] += gv * to_f<T>(u[i]);
+  }
+}
+template <>
+__global__ void cross_bwd_pointwise_kernel<double>(const double* __restrict__ g, const double* __restrict__ x0,
+                                                   const double* __restrict__ u, double* __restrict__ gu,
+                                                   float* __restrict__ dx0, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    gu[i] = g[i] * x0[i];
+    dx0[i] += (float)(g[i] * u[i]);
+  }
+}
+
+template <typename T>
+__global__ void sgd_dense_kernel(T* __restrict__ w, const float* __restrict__ g, int64_t n, float lr) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = from_d<T>(to_d<T>(w[i]) - (double)lr * (double)g[i]);
+}
+
+template <typename A, typename B>
+__global__ void convert_kernel(const A* __restrict__ a, B* __restrict__ b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = from_d<B>(to_d<A>(a[i]));
+}
+
+template <typename A>
+int convert_to(const void* src, void* dst, int32_t dto, int64_t n, cudaStream_t s) {
+  unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, 256), DMT_NUM_SMS * 16);
+  switch (dto) {
+    case DMT_F32: convert_kernel<A, float><<<grid, 256, 0, s>>>((const A*)src, (float*)dst, n); break;
+    case DMT_BF16: convert_kernel<A, __nv_bfloat16><<<grid, 256, 0, s>>>((const A*)src, (__nv_bfloat16*)dst, n); break;
+    case DMT_F64: convert_kernel<A, double><<<grid, 256, 0, s>>>((const A*)src, (double*)dst, n); break;
+    case DMT_F16: convert_kernel<A, __half><<<grid, 256, 0, s>>>((const A*)src, (__half*)dst, n); break;
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+}  // namespace dmt
+
+extern "C" {
+
+int dmt_assemble(const dmt_assemble_block* blocks, int32_t num_blocks, int32_t max_width, const dmt_src* srcs,
+                 int64_t rows, void* dst, int64_t dst_ld, int32_t dtype, dmt_stream_t stream) {
+  // The vector path is only taken when the caller guarantees 16-byte
+  // alignment of every block (flagged via a negative max_width).
+  bool vec_ok = max_width < 0;
+  if (vec_ok) max_width = -max_width;
+  if (num_blocks < 0 || rows < 0) return DMT_ERR_DOMAIN;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case DMT_F32: return dmt::launch_assemble<float>(blocks, num_blocks, max_width, srcs, rows, dst, dst_ld, s, vec_ok);
+    case DMT_BF16:
+      return dmt::launch_assemble<__nv_bfloat16>(blocks, num_blocks, max_width, srcs, rows, dst, dst_ld, s, vec_ok);
+    case DMT_F64: return dmt::launch_assemble<double>(blocks, num_blocks, max_width, srcs, rows, dst, dst_ld, s, vec_ok);
+    case DMT_F16: return dmt::launch_assemble<__half>(blocks, num_blocks, max_width, srcs, rows, dst, dst_ld, s, vec_ok);
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+}
+
+int dmt_batched_copy(const dmt_copy* copies, int32_t n, int64_t max_bytes, dmt_stream_t stream) {
+  if (n < 0) return DMT_ERR_DOMAIN;
+  if (n == 0 || max_bytes <= 0) return DMT_OK;
+  if (n > 65535) return DMT_ERR_UNSUPPORTED;
+  unsigned gx = (unsigned)std::min<int64_t>(dmt::ceil_div(max_bytes, 16 * 256), 1024);
+  dmt::batched_copy_kernel<<<dim3(gx, n), 256, 0, (cudaStream_t)stream>>>(copies);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_batched_copy2d(const dmt_copy2d* copies, int32_t n, int32_t elem_bytes, int64_t max_elems,
+                       dmt_stream_t stream) {
+  if (n < 0) return DMT_ERR_DOMAIN;
+  if (n == 0 || max_elems <= 0) return DMT_OK;
+  if (n > 65535) return DMT_ERR_UNSUPPORTED;
+  unsigned gx = (unsigned)std::min<int64_t>(dmt::ceil_div(max_elems, 256), 2048);
+  dim3 grid(gx, n);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (elem_bytes) {
+    case 2: dmt::batched_copy2d_kernel<uint16_t><<<grid, 256, 0, s>>>(copies); break;
+    case 4: dmt::batched_copy2d_kernel<uint32_t><<<grid, 256, 0, s>>>(copies); break;
+    case 8: dmt::batched_copy2d_kernel<uint64_t><<<grid, 256, 0, s>>>(copies); break;
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_transpose(const void* in, int64_t rows, int64_t cols, int64_t ld_in, void* out, int64_t ld_out,
+                  int32_t dtype, dmt_stream_t stream) {
+  if (rows == 0 || cols == 0) return DMT_OK;
+  dim3 grid((unsigned)dmt::ceil_div(cols, 32), (unsigned)dmt::ceil_div(rows, 32));
+  dim3 block(32, 8);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case DMT_F32: dmt::transpose_kernel<float><<<grid, block, 0, s>>>((const float*)in, rows, cols, ld_in, (float*)out, ld_out); break;
+    case DMT_BF16:
+    case DMT_F16:
+      dmt::transpose_kernel<uint16_t><<<grid, block, 0, s>>>((const uint16_t*)in, rows, cols, ld_in, (uint16_t*)out, ld_out);
+      break;
+    case DMT_F64: dmt::transpose_kernel<double><<<grid, block, 0, s>>>((const double*)in, rows, cols, ld_in, (double*)out, ld_out); break;
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+static inline int colsum_parts(int64_t rows) {
+  return (int)std::min<int64_t>(std::max<int64_t>(1, rows / 256), 64);
+}
+
+size_t dmt_column_sum_workspace_size(int64_t rows, int64_t cols) {
+  return sizeof(double) * (size_t)colsum_parts(rows) * (size_t)(cols > 0 ? cols : 1);
+}
+
+int dmt_column_sum(const void* in, int64_t rows, int64_t cols, int64_t ld, float* out, int32_t dtype,
+                   void* workspace, size_t workspace_bytes, dmt_stream_t stream) {
+  if (cols == 0) return DMT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int nparts = colsum_parts(rows);
+  int64_t rows_per = dmt::ceil_div(std::max<int64_t>(rows, 1), nparts);
+  if (workspace_bytes < dmt_column_sum_workspace_size(rows, cols)) return DMT_ERR_DOMAIN;
+  double* g_colsum_scratch = (double*)workspace;
+  dim3 grid((unsigned)dmt::ceil_div(cols, 256), nparts);
+  switch (dtype) {
+    case DMT_F32: dmt::colsum_partial<float><<<grid, 256, 0, s>>>((const float*)in, rows, cols, ld, rows_per, g_colsum_scratch); break;
+    case DMT_BF16: dmt::colsum_partial<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)in, rows, cols, ld, rows_per, g_colsum_scratch); break;
+    case DMT_F64: dmt::colsum_partial<double><<<grid, 256, 0, s>>>((const double*)in, rows, cols, ld, rows_per, g_colsum_scratch); break;
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+  dmt::colsum_final<<<(unsigned)dmt::ceil_div(cols, 256), 256, 0, s>>>(g_colsum_scratch, cols, nparts, out);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_cross_bwd_pointwise(const void* g, const void* x0, const void* u, void* gu, float* dx0, int64_t n,
+                            int32_t dtype, dmt_stream_t stream) {
+  if (n == 0) return DMT_OK;
+  unsigned grid = (unsigned)std::min<int64_t>(dmt::ceil_div(n, 256), DMT_NUM_SMS * 16);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case DMT_F32: dmt::cross_bwd_pointwise_kernel<float><<<grid, 256, 0, s>>>((const float*)g, (const float*)x0, (const float*)u, (float*)gu, dx0, n); break;
+    case DMT_BF16: dmt::cross_bwd_pointwise_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)g, (const __nv_bfloat16*)x0, (const __nv_bfloat16*)u, (__nv_bfloat16*)gu, dx0, n); break;
+    case DMT_F64: dmt::cross_bwd_pointwise_kernel<double><<<grid, 256, 0, s>>>((const double*)g, (const double*)x0, (const double*)u, (double*)gu, dx0, n); break;
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_sgd_dense(void* w, const float* g, int64_t n, float lr, int32_t dtype, dmt_stream_t stream) {
+  if (n == 0) return DMT_OK;
+  unsigned grid = (unsigned)std::min<int64_t>(dmt::ceil_div(n, 256), DMT_NUM_SMS * 16);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case DMT_F32: dmt::sgd_dense_kernel<float><<<grid, 256, 0, s>>>((float*)w, g, n, lr); break;
+    case DMT_BF16: dmt::sgd_dense_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)w, g, n, lr); break;
+    case DMT_F64: dmt::sgd_dense_kernel<double><<<grid, 256, 0, s>>>((double*)w, g, n, lr); break;
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_convert(const void* src, int32_t dtype_in, void* dst, int32_t dtype_out, int64_t n, dmt_stream_t stream) {
+  if (n == 0) return DMT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype_in) {
+    case DMT_F32: return dmt::convert_to<float>(src, dst, dtype_out, n, s);
+    case DMT_BF16: return dmt::convert_to<__nv_bfloat16>(src, dst, dtype_out, n, s);
+    case DMT_F64: return dmt::convert_to<double>(src, dst, dtype_out, n, s);
+    case DMT_F16: return dmt::convert_to<__half>(src, dst, dtype_out, n, s);
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,496 @@
+// Tower-module GEMMs on the 5th-generation tensor cores.
+//
+//   D[m, n] = epilogue( sum_k A[m, k] * B[n, k] )       A, B K-major
+//
+// Reference math: tm_dlrm_forward (towersim/towermod.py:110-129: x W^T + b),
+// crossnet_layer (towermod.py:132-139: x0 * (xl W^T + b) + xl) and the DCN
+// projection (towermod.py:158).  Weights are (out, in) row-major exactly like
+// the reference, i.e. already K-major for the B operand.
+//
+// Kernel anatomy (one CTA per SM, persistent over output tiles):
+//   warp 0      : TMA producer  -- cp.async.bulk.tensor 2D, SWIZZLE_128B, an
+//                 mbarrier full/empty ring of STAGES operand slots
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer; commits
+//                 free smem slots and publish finished accumulators
+//   warps 2..5  : epilogue -- tcgen05.ld TMEM -> registers, bias / crossnet
+//                 gate / accumulate, convert, store; warp w owns TMEM lanes
+//                 32*(w%4) .. +31 (one output row per thread)
+// Two TMEM accumulators (2 x BN fp32 columns) let the epilogue of tile i
+// overlap the MMAs of tile i+1.
+//
+// Precision: bf16/f16 operands use kind::f16 (fp32 accumulate).  fp32
+// operands use kind::tf32 with the 3xTF32 split (a = a_hi + a_lo, products
+// hi*hi + hi*lo + lo*hi accumulate in TMEM), which restores ~fp32 accuracy
+// (rtol 1e-5 parity bar of the north star).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace dmt {
+namespace gemm {
+
+constexpr int kThreads = 192;  // 6 warps
+constexpr int kBlockM = 128;
+constexpr int kAtomBytes = 128;  // one SWIZZLE_128B row = BLOCK_K bytes per stage
+constexpr int kUmmaKBytes = 32;  // K bytes consumed by one tcgen05.mma (16 x bf16 / 8 x tf32)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+template <int KIND>  // 0 = f16/bf16, 1 = tf32
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                     uint32_t accumulate) {
+  if constexpr (KIND == 0) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  }
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 lanes x 32 columns of 32-bit TMEM -> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// SM100 shared-memory matrix descriptor, K-major, SWIZZLE_128B:
+//   [0,14) start>>4  [16,30) LBO>>4 (unused for swizzled K-major)
+//   [32,46) SBO>>4 = 1024 B between 8-row core groups   [46,48) version = 1
+//   [61,64) layout = 2 (SWIZZLE_128B)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor (kind::f16 / kind::tf32), both operands K-major:
+//   [4,6) D fmt = 1 (f32)  [7,10) A fmt  [10,13) B fmt  [17,23) N>>3  [24,29) M>>4
+__host__ __device__ constexpr uint32_t make_idesc(int ab_fmt, int m, int n) {
+  return (1u << 4) | ((uint32_t)ab_fmt << 7) | ((uint32_t)ab_fmt << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(m >> 4) << 24);
+}
+
+struct Params {
+  int64_t m, n, k;
+  int64_t ld_d, ld_x, rows_per_group, ld_group;
+  void* d;
+  const float* bias;
+  const void* x0;
+  const void* xl;
+  void* aux;
+  float beta;
+  int out_dtype;
+  int in_dtype;
+  int epilogue;
+  int vec_store;
+};
+
+template <typename TO>
+__device__ __forceinline__ void store_row32(TO* p, const float* v, int ncols, bool vec) {
+  if (vec && ncols == 32) {
+    if constexpr (sizeof(TO) == 4) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 x;
+        TO* h = reinterpret_cast<TO*>(&x);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) h[j] = from_f<TO>(v[i + j]);
+        *reinterpret_cast<uint4*>(p + i) = x;
+      }
+    }
+  } else {
+    for (int i = 0; i < ncols; ++i) p[i] = from_f<TO>(v[i]);
+  }
+}
+
+template <typename TX>
+__device__ __forceinline__ void load_row32(const TX* p, float* v, int ncols) {
+  for (int i = 0; i < ncols; ++i) v[i] = to_f<TX>(p[i]);
+}
+
+// BN: tile N (64/128/256); NOPS: 1 (plain) or 3 (3xTF32); KIND: 0 f16-family, 1 tf32
+template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+            const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_lo,
+            const Params p, uint32_t idesc) {
+  constexpr int A_BYTES = kBlockM * kAtomBytes;
+  constexpr int B_BYTES = BN * kAtomBytes;
+  constexpr int NSETS = (NOPS == 3) ? 2 : 1;  // hi (+ lo) operand copies
+  constexpr int STAGE_BYTES = NSETS * (A_BYTES + B_BYTES);
+  constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tiles_m = ceil_div(p.m, kBlockM), tiles_n = ceil_div(p.n, BN);
+  const int64_t num_tiles = tiles_m * tiles_n;
+  const int num_kb = (int)ceil_div(p.k * (int64_t)sizeof(TIN), kAtomBytes);
+  constexpr int K_ELEMS = kAtomBytes / sizeof(TIN);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (int)((tile / tiles_n) * kBlockM);
+        const int n0 = (int)((tile % tiles_n) * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(sa, &map_a, &full[stage], kb * K_ELEMS, m0);
+          tma_load_2d(sb, &map_b, &full[stage], kb * K_ELEMS, n0);
+          if constexpr (NSETS == 2) {
+            uint8_t* sa2 = sb + B_BYTES;
+            uint8_t* sb2 = sa2 + A_BYTES;
+            tma_load_2d(sa2, &map_a_lo, &full[stage], kb * K_ELEMS, m0);
+            tma_load_2d(sb2, &map_b_lo, &full[stage], kb * K_ELEMS, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          const uint64_t da = make_desc(smem_u32(sa));
+          const uint64_t db = make_desc(smem_u32(sb));
+#pragma unroll
+          for (int kk = 0; kk < kAtomBytes / kUmmaKBytes; ++kk) {
+            const uint64_t adv = (uint64_t)((kk * kUmmaKBytes) >> 4);
+            const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
+            umma<KIND>(tmem_d, da + adv, db + adv, idesc, accum);
+            if constexpr (NSETS == 2) {
+              uint8_t* sa2 = sb + B_BYTES;
+              uint8_t* sb2 = sa2 + A_BYTES;
+              const uint64_t da2 = make_desc(smem_u32(sa2));
+              const uint64_t db2 = make_desc(smem_u32(sb2));
+              umma<KIND>(tmem_d, da + adv, db2 + adv, idesc, 1u);  // hi * lo
+              umma<KIND>(tmem_d, da2 + adv, db + adv, idesc, 1u);  // lo * hi
+            }
+          }
+          umma_commit(&empty[stage]);  // smem slot reusable once these MMAs retire
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);  // accumulator complete
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int64_t m0 = (tile / tiles_n) * kBlockM;
+      const int64_t n0 = (tile % tiles_n) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row = m0 + q * 32 + lane;
+      const bool row_ok = row < p.m;
+      TO* drow = nullptr;
+      if (row_ok)
+        drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), v);
+        const int64_t col = n0 + c;
+        const int64_t rem = p.n - col;
+        const int ncols = rem <= 0 ? 0 : (rem < 32 ? (int)rem : 32);
+        if (!row_ok || ncols == 0) continue;
+        if (p.epilogue == DMT_EPI_BIAS || p.epilogue == DMT_EPI_CROSS) {
+          for (int i = 0; i < ncols; ++i) v[i] += p.bias[col + i];
+        }
+        if (p.epilogue == DMT_EPI_CROSS) {
+          float x0v[32], xlv[32];
+          const TIN* x0p = reinterpret_cast<const TIN*>(p.x0) + row * p.ld_x + col;
+          const TIN* xlp = reinterpret_cast<const TIN*>(p.xl) + row * p.ld_x + col;
+          load_row32<TIN>(x0p, x0v, ncols);
+          load_row32<TIN>(xlp, xlv, ncols);
+          if (p.aux) store_row32<TIN>(reinterpret_cast<TIN*>(p.aux) + row * p.ld_x + col, v, ncols, false);
+          for (int i = 0; i < ncols; ++i) v[i] = x0v[i] * v[i] + xlv[i];
+        } else if (p.epilogue == DMT_EPI_ACC) {
+          float old[32];
+          load_row32<TO>(drow + col, old, ncols);
+          for (int i = 0; i < ncols; ++i) v[i] += p.beta * old[i];
+        }
+        store_row32<TO>(drow + col, v, ncols, p.vec_store != 0);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- host ------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int64_t ld, int dtype,
+                     int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  CUtensorMapDataType t;
+  size_t es = dtype_size(dtype);
+  switch (dtype) {
+    case DMT_BF16: t = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16; break;
+    case DMT_F16: t = CU_TENSOR_MAP_DATA_TYPE_FLOAT16; break;
+    case DMT_F32: t = CU_TENSOR_MAP_DATA_TYPE_FLOAT32; break;
+    default: return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {(cuuint32_t)(kAtomBytes / es), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, t, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO>
+static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cudaStream_t s) {
+  constexpr int NSETS = (NOPS == 3) ? 2 : 1;
+  constexpr int STAGE_BYTES = NSETS * (kBlockM + BN) * kAtomBytes;
+  constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(SMEM <= 232448, "smem");
+  CUtensorMap ma, mb, mal, mbl;
+  if (!make_map(&ma, a->a, a->m, a->k, a->lda, a->in_dtype, kBlockM)) return DMT_ERR_CUDA;
+  if (!make_map(&mb, a->b, a->n, a->k, a->ldb, a->in_dtype, BN)) return DMT_ERR_CUDA;
+  if (NSETS == 2) {
+    if (!make_map(&mal, a_lo, a->m, a->k, a->lda, a->in_dtype, kBlockM)) return DMT_ERR_CUDA;
+    if (!make_map(&mbl, b_lo, a->n, a->k, a->ldb, a->in_dtype, BN)) return DMT_ERR_CUDA;
+  } else {
+    mal = ma;
+    mbl = mb;
+  }
+  Params p;
+  p.m = a->m; p.n = a->n; p.k = a->k;
+  p.ld_d = a->ld_d; p.ld_x = a->ld_x;
+  p.rows_per_group = a->rows_per_group > 0 ? a->rows_per_group : a->m + 1;
+  p.ld_group = a->ld_group;
+  p.d = a->d; p.bias = a->bias; p.x0 = a->x0; p.xl = a->xl; p.aux = a->aux;
+  p.beta = a->beta; p.out_dtype = a->out_dtype; p.in_dtype = a->in_dtype; p.epilogue = a->epilogue;
+  size_t eo = dtype_size(a->out_dtype);
+  p.vec_store = ((uintptr_t)a->d % 16 == 0) && ((a->ld_d * eo) % 16 == 0) && ((a->ld_group * eo) % 16 == 0);
+  auto kern = gemm_kernel<BN, NOPS, KIND, STAGES, TIN, TO>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
+      return DMT_ERR_CUDA;
+    attr_set = true;
+  }
+  int64_t tiles = ceil_div(a->m, kBlockM) * ceil_div(a->n, BN);
+  int grid = (int)std::min<int64_t>(tiles, DMT_NUM_SMS);
+  const int fmt = (KIND == 1) ? 2 : (std::is_same<TIN, __half>::value ? 0 : 1);
+  uint32_t idesc = make_idesc(fmt, kBlockM, BN);
+  kern<<<grid, kThreads, SMEM, s>>>(ma, mb, mal, mbl, p, idesc);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+template <typename TIN, typename TO>
+static int dispatch_n(const dmt_gemm_args* a, const void* alo, const void* blo, cudaStream_t s) {
+  if constexpr (std::is_same<TIN, float>::value) {
+    if (a->n <= 64) return launch<64, 3, 1, 4, TIN, TO>(a, alo, blo, s);
+    return launch<128, 3, 1, 3, TIN, TO>(a, alo, blo, s);
+  } else {
+    if (a->n <= 64) return launch<64, 1, 0, 8, TIN, TO>(a, alo, blo, s);
+    if (a->n <= 128) return launch<128, 1, 0, 6, TIN, TO>(a, alo, blo, s);
+    return launch<256, 1, 0, 4, TIN, TO>(a, alo, blo, s);
+  }
+}
+
+template <typename TIN>
+static int dispatch_out(const dmt_gemm_args* a, const void* alo, const void* blo, cudaStream_t s) {
+  switch (a->out_dtype) {
+    case DMT_F32: return dispatch_n<TIN, float>(a, alo, blo, s);
+    case DMT_BF16: return dispatch_n<TIN, __nv_bfloat16>(a, alo, blo, s);
+    case DMT_F16: return dispatch_n<TIN, __half>(a, alo, blo, s);
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+}
+
+__global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo,
+                                  int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float v = x[i];
+    float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+
+}  // namespace gemm
+}  // namespace dmt
+
+extern "C" {
+
+int dmt_gemm_ex(const dmt_gemm_args* args, const void* a_lo, const void* b_lo, dmt_stream_t stream) {
+  using namespace dmt;
+  if (!args) return DMT_ERR_DOMAIN;
+  const dmt_gemm_args* a = args;
+  if (a->m < 0 || a->n < 0 || a->k < 0) return DMT_ERR_SHAPE;
+  if (a->m == 0 || a->n == 0) return DMT_OK;
+  if (a->k == 0) return DMT_ERR_SHAPE;  // caller handles the bias-only case
+  if (a->m > INT32_MAX || a->n > INT32_MAX || a->k > INT32_MAX) return DMT_ERR_UNSUPPORTED;
+  size_t es = dtype_size(a->in_dtype);
+  if (es == 0 || a->in_dtype == DMT_F64) return DMT_ERR_UNSUPPORTED;
+  // TMA: 16-byte aligned base and row strides
+  if (((uintptr_t)a->a & 15) || ((uintptr_t)a->b & 15) || (a->lda * es) % 16 || (a->ldb * es) % 16)
+    return DMT_ERR_UNSUPPORTED;
+  if ((a->epilogue == DMT_EPI_BIAS || a->epilogue == DMT_EPI_CROSS) && !a->bias) return DMT_ERR_DOMAIN;
+  if (a->epilogue == DMT_EPI_CROSS && (!a->x0 || !a->xl)) return DMT_ERR_DOMAIN;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (a->in_dtype) {
+    case DMT_BF16: return gemm::dispatch_out<__nv_bfloat16>(a, nullptr, nullptr, s);
+    case DMT_F16: return gemm::dispatch_out<__half>(a, nullptr, nullptr, s);
+    case DMT_F32:
+      if (!a_lo || !b_lo) return DMT_ERR_DOMAIN;
+      if (((uintptr_t)a_lo & 15) || ((uintptr_t)b_lo & 15)) return DMT_ERR_UNSUPPORTED;
+      return gemm::dispatch_out<float>(a, a_lo, b_lo, s);
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+}
+
+int dmt_gemm(const dmt_gemm_args* args, dmt_stream_t stream) { return dmt_gemm_ex(args, nullptr, nullptr, stream); }
+
+int dmt_split_tf32(const float* x, float* hi, float* lo, int64_t n, dmt_stream_t stream) {
+  if (n == 0) return DMT_OK;
+  unsigned grid = (unsigned)std::min<int64_t>(dmt::ceil_div(n, 256), DMT_NUM_SMS * 16);
+  dmt::gemm::split_tf32_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, hi, lo, n);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,188 @@
+// KJT plumbing: lengths -> offsets scan and step-a bucketing.
+//
+// Reference: step a of _distribute_and_lookup ships, for every (src, owner),
+// the full bag list of each shard the owner holds, bundled in shard-id order
+// (towersim/exchange.py:162-178).  On the device that is a jagged gather of
+// per-feature (lengths, values) segments into per-owner send slots; the
+// all-to-all that follows is NCCL (or an in-process copy) on these buffers.
+#include "common.cuh"
+
+namespace dmt {
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 8;  // per thread
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// Block-wide exclusive scan of per-thread sums (int64) via warp shuffles.
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* total) {
+  __shared__ int64_t warp_sums[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    int64_t s = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) warp_sums[lane] = s;  // inclusive
+  }
+  __syncthreads();
+  int64_t warp_prefix = warp ? warp_sums[warp - 1] : 0;
+  if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
+  int64_t excl = warp_prefix + x - v;
+  __syncthreads();
+  return excl;
+}
+
+// Pass 1: per-tile sums.
+__global__ void scan_tile_sums(const int32_t* __restrict__ len, int64_t n, int64_t* __restrict__ tile_sums) {
+  int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + (int64_t)i * kScanThreads + threadIdx.x;
+    if (idx < n) s += len[idx];
+  }
+  int64_t total;
+  block_exclusive_scan(s, &total);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+// Pass 2: exclusive scan of tile sums (single block, loops if many tiles).
+__global__ void scan_tile_prefix(int64_t* __restrict__ tile_sums, int64_t ntiles) {
+  int64_t carry = 0;
+  for (int64_t base = 0; base < ntiles; base += kScanThreads) {
+    int64_t idx = base + threadIdx.x;
+    int64_t v = idx < ntiles ? tile_sums[idx] : 0;
+    int64_t total;
+    int64_t ex = block_exclusive_scan(v, &total);
+    if (idx < ntiles) tile_sums[idx] = carry + ex;
+    carry += total;
+    __syncthreads();
+  }
+}
+
+// Pass 3: each tile rescans its items with the tile prefix.  Thread t owns
+// kScanItems consecutive items so the scan is a plain sequential prefix.
+__global__ void scan_apply(const int32_t* __restrict__ len, int64_t n, const int64_t* __restrict__ tile_prefix,
+                           int64_t* __restrict__ out) {
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int32_t v[kScanItems];
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + i;
+    v[i] = idx < n ? len[idx] : 0;
+    s += v[i];
+  }
+  int64_t ex = block_exclusive_scan(s, nullptr) + tile_prefix[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + i;
+    if (idx < n) out[idx] = ex;
+    ex += v[i];
+    if (idx == n - 1) out[n] = ex;
+  }
+}
+
+__global__ void zero_one(int64_t* p) { p[0] = 0; }
+
+// Bucketize: grid.y = slot, grid.x strides over the slot's lengths + values.
+__global__ void bucketize_kernel(const int32_t* __restrict__ lengths, const int64_t* __restrict__ offsets,
+                                 const int32_t* __restrict__ values, int32_t B,
+                                 const int32_t* __restrict__ slot_feature,
+                                 const int64_t* __restrict__ slot_off, int32_t* __restrict__ out_lengths,
+                                 int32_t* __restrict__ out_values) {
+  const int s = blockIdx.y;
+  const int f = slot_feature[s];
+  const int64_t vbeg = offsets[(int64_t)f * B];
+  const int64_t vend = offsets[(int64_t)(f + 1) * B];
+  const int64_t nnz = vend - vbeg;
+  const int64_t dst = slot_off[s];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B; i += stride)
+    out_lengths[(int64_t)s * B + i] = lengths[(int64_t)f * B + i];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride)
+    out_values[dst + i] = __ldg(values + vbeg + i);
+}
+
+__global__ void slot_offsets_kernel(const int64_t* __restrict__ offsets, int32_t B, int32_t num_slots,
+                                    const int32_t* __restrict__ slot_feature, int64_t* __restrict__ out) {
+  // single block; num_slots is small (shards per world)
+  int64_t carry = 0;
+  for (int base = 0; base < num_slots; base += blockDim.x) {
+    int s = base + threadIdx.x;
+    int64_t v = 0;
+    if (s < num_slots) {
+      int f = slot_feature[s];
+      v = offsets[(int64_t)(f + 1) * B] - offsets[(int64_t)f * B];
+    }
+    int64_t total;
+    int64_t ex = block_exclusive_scan(v, &total);
+    if (s < num_slots) out[s] = carry + ex;
+    carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[num_slots] = carry;
+}
+
+}  // namespace dmt
+
+extern "C" {
+
+size_t dmt_lengths_to_offsets_workspace_size(int64_t n) {
+  return sizeof(int64_t) * (size_t)(dmt::ceil_div(n, dmt::kScanTile) + 1);
+}
+
+int dmt_lengths_to_offsets(const int32_t* lengths, int64_t n, int64_t* offsets, void* scratch,
+                           dmt_stream_t stream) {
+  if (n < 0) return DMT_ERR_DOMAIN;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) {
+    dmt::zero_one<<<1, 1, 0, s>>>(offsets);
+    DMT_CHECK_LAUNCH();
+    return DMT_OK;
+  }
+  int64_t ntiles = dmt::ceil_div(n, dmt::kScanTile);
+  int64_t* tiles = (int64_t*)scratch;
+  dmt::scan_tile_sums<<<(unsigned)ntiles, dmt::kScanThreads, 0, s>>>(lengths, n, tiles);
+  dmt::scan_tile_prefix<<<1, dmt::kScanThreads, 0, s>>>(tiles, ntiles);
+  dmt::scan_apply<<<(unsigned)ntiles, dmt::kScanThreads, 0, s>>>(lengths, n, tiles, offsets);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_kjt_bucketize(const int32_t* lengths, const int64_t* offsets, const int32_t* values, int32_t B,
+                      int32_t num_slots, const int32_t* slot_feature, const int64_t* slot_value_offset,
+                      int32_t* out_lengths, int32_t* out_values, dmt_stream_t stream) {
+  if (B < 0 || num_slots < 0) return DMT_ERR_DOMAIN;
+  if (num_slots == 0 || B == 0) return DMT_OK;
+  if (num_slots > 65535) return DMT_ERR_UNSUPPORTED;
+  dim3 grid(64, num_slots);
+  dmt::bucketize_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(lengths, offsets, values, B, slot_feature,
+                                                                 slot_value_offset, out_lengths, out_values);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_kjt_slot_offsets(const int64_t* offsets, int32_t B, int32_t num_slots, const int32_t* slot_feature,
+                         int64_t* slot_value_offset, dmt_stream_t stream) {
+  if (num_slots < 0 || B < 0) return DMT_ERR_DOMAIN;
+  dmt::slot_offsets_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(offsets, B, num_slots, slot_feature,
+                                                                  slot_value_offset);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+const char* dmt_version(void) { return "libdmt 0.1.0 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,144 @@
+"""Collective backends of the exchange: NCCL (one process per GPU) and an
+in-process loopback that hosts several simulated ranks on one device.
+
+Both implement the reference's all-to-all semantics (towersim/simnet.py:117-146):
+member j of ``group`` receives one payload per source, in group order.  Payloads
+here are flat device buffers with per-destination element splits; the
+receiver's buffer is the concatenation of the sources' pieces in group order.
+"""
+
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import torch
+
+from . import kernels as K
+from .errors import ProtocolError
+from .simnet import CommTrace
+
+
+def _offsets(splits: Sequence[int]) -> list[int]:
+    out, acc = [], 0
+    for s in splits:
+        out.append(acc)
+        acc += int(s)
+    return out
+
+
+class Fabric:
+    local_ranks: list[int]
+    world_size: int
+
+    def alltoallv(self, group: Sequence[int], label: str, send: dict, send_splits: dict, recv: dict,
+                  recv_splits: dict, trace: Optional[CommTrace] = None, elem_bytes: int = 4) -> None:
+        raise NotImplementedError
+
+    def exchange_counts(self, group: Sequence[int], counts: dict) -> dict:
+        """counts[r][j] = elements r sends to group[j]  ->  recv[r][j] from group[j]."""
+        raise NotImplementedError
+
+    def all_reduce_(self, group: Sequence[int], tensors: dict) -> None:
+        raise NotImplementedError
+
+
+class LoopbackFabric(Fabric):
+    """All G ranks in this process on one device; delivery = one batched-copy
+    kernel launch per collective (dmt_batched_copy)."""
+
+    def __init__(self, world_size: int, device=None):
+        self.world_size = world_size
+        self.local_ranks = list(range(world_size))
+        self.device = device or torch.device("cuda")
+
+    def alltoallv(self, group, label, send, send_splits, recv, recv_splits, trace=None, elem_bytes=4):
+        n = len(group)
+        copies = []
+        for i, src in enumerate(group):
+            if len(send_splits[src]) != n:
+                raise ProtocolError(f"rank {src} supplied {len(send_splits[src])} splits for {label!r}, expected {n}")
+        for j, dst in enumerate(group):
+            roffs = _offsets(recv_splits[dst])
+            for i, src in enumerate(group):
+                cnt = int(send_splits[src][j])
+                if cnt != int(recv_splits[dst][i]):
+                    raise ProtocolError(f"{label!r}: {src}->{dst} sends {cnt} but {recv_splits[dst][i]} expected")
+                if trace is not None:
+                    trace.record_elements(label, src, dst, cnt, elem_bytes)
+                if cnt == 0:
+                    continue
+                soff = _offsets(send_splits[src])[j]
+                s, d = send[src], recv[dst]
+                es = s.element_size()
+                copies.append((s.data_ptr() + soff * es, d.data_ptr() + roffs[i] * es, cnt * es))
+        K.CopyTable(copies, self.device).run()
+
+    def exchange_counts(self, group, counts):
+        return {dst: [counts[src][j] for src in group] for j, dst in enumerate(group)}
+
+    def all_reduce_(self, group, tensors):
+        # every rank of a loopback tower shares one module; nothing to do
+        return None
+
+
+class NcclFabric(Fabric):
+    """One rank per process; torch.distributed NCCL groups for the world, each
+    tower (colour r // W) and each peer class (colour r % W), created once in a
+    fixed order on every rank."""
+
+    def __init__(self, world_size: int, rank: int, W: int, backend_device=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.world_size = world_size
+        self.rank = rank
+        self.local_ranks = [rank]
+        self.W = W
+        self.T = world_size // W
+        self.device = backend_device or torch.device("cuda", torch.cuda.current_device())
+        self.groups = {tuple(range(world_size)): None}  # None = default (world) group
+        for t in range(self.T):
+            ranks = tuple(range(t * W, (t + 1) * W))
+            g = dist.new_group(list(ranks)) if len(ranks) < world_size else None
+            self.groups[ranks] = g
+        for c in range(W):
+            ranks = tuple(t * W + c for t in range(self.T))
+            g = dist.new_group(list(ranks)) if 1 < len(ranks) < world_size else None
+            self.groups.setdefault(ranks, g)
+
+    def _pg(self, group):
+        key = tuple(group)
+        if key not in self.groups:
+            self.groups[key] = self.dist.new_group(list(key))
+        return self.groups[key]
+
+    def alltoallv(self, group, label, send, send_splits, recv, recv_splits, trace=None, elem_bytes=4):
+        r = self.rank
+        if trace is not None:
+            for j, dst in enumerate(group):
+                trace.record_elements(label, r, dst, int(send_splits[r][j]), elem_bytes)
+        if len(group) == 1:
+            n = int(send_splits[r][0])
+            if n:
+                recv[r][:n].copy_(send[r][:n])
+            return
+        self.dist.all_to_all_single(recv[r][: sum(recv_splits[r])], send[r][: sum(send_splits[r])],
+                                    output_split_sizes=[int(x) for x in recv_splits[r]],
+                                    input_split_sizes=[int(x) for x in send_splits[r]],
+                                    group=self._pg(group))
+
+    def exchange_counts(self, group, counts):
+        r = self.rank
+        if len(group) == 1:
+            return {r: list(counts[r])}
+        s = torch.tensor(counts[r], dtype=torch.int64, device=self.device)
+        o = torch.empty_like(s)
+        self.dist.all_to_all_single(o, s, group=self._pg(group))
+        return {r: o.cpu().tolist()}  # host sync: ragged step-a value splits
+
+    def all_reduce_(self, group, tensors):
+        if len(group) == 1:
+            return
+        pg = self._pg(group)
+        for t in tensors.values():
+            self.dist.all_reduce(t, group=pg)

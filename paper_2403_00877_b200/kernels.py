@@ -1,0 +1,336 @@
+"""Typed torch-facing wrappers over the libdmt C ABI (include/dmt.h).
+
+Each wrapper takes device tensors, validates shapes/dtypes on the host, calls
+the C entry point on the current CUDA stream and maps non-zero status codes to
+the reference exception classes.  No wrapper has a CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib as L
+from .errors import DomainError, ShapeError, TableLookupError
+
+
+def _dt(t: torch.Tensor) -> int:
+    try:
+        return L.TORCH_DT[t.dtype]
+    except KeyError:
+        raise DomainError(f"unsupported dtype {t.dtype}") from None
+
+
+def device_table(ctype, items: Sequence, device) -> tuple[torch.Tensor, object]:
+    """Upload a list of ctypes structs; returns (device bytes, host array)."""
+    arr = (ctype * max(1, len(items)))()
+    for i, it in enumerate(items):
+        arr[i] = it
+    nbytes = C.sizeof(ctype) * max(1, len(items))
+    buf = bytearray(C.string_at(C.addressof(arr), nbytes))
+    dev = torch.frombuffer(buf, dtype=torch.uint8).to(device)
+    return dev, arr
+
+
+# ------------------------------------------------------------------ KJT ----
+def lengths_to_offsets(lengths: torch.Tensor) -> torch.Tensor:
+    if lengths.dtype != torch.int32 or not lengths.is_cuda:
+        raise DomainError("lengths must be a CUDA int32 tensor")
+    lengths = lengths.contiguous()
+    n = lengths.numel()
+    out = torch.empty(n + 1, dtype=torch.int64, device=lengths.device)
+    ws = torch.empty(max(1, L.lib().dmt_lengths_to_offsets_workspace_size(n)), dtype=torch.uint8,
+                     device=lengths.device)
+    L.check(L.lib().dmt_lengths_to_offsets(lengths.data_ptr(), n, out.data_ptr(), ws.data_ptr(), L.stream_ptr()),
+            "dmt_lengths_to_offsets")
+    return out
+
+
+def kjt_bucketize(lengths, offsets, values, B: int, slot_feature: torch.Tensor,
+                  slot_value_offset: torch.Tensor, out_lengths: torch.Tensor, out_values: torch.Tensor) -> None:
+    n_slots = slot_feature.numel()
+    L.check(L.lib().dmt_kjt_bucketize(lengths.data_ptr(), offsets.data_ptr(), values.data_ptr(), B, n_slots,
+                                      slot_feature.data_ptr(), slot_value_offset.data_ptr(),
+                                      out_lengths.data_ptr(), out_values.data_ptr(), L.stream_ptr()),
+            "dmt_kjt_bucketize")
+
+
+# --------------------------------------------------------- pooled lookup ----
+@dataclass
+class Segment:
+    """One lookup segment (dmt_lookup_segment)."""
+
+    weights: torch.Tensor      # shard rows (rows, ld) -- row r at weights[r - row_begin]
+    out: torch.Tensor          # base tensor of the output
+    out_offset: int            # element offset of bag 0's row in `out`
+    out_ld: int
+    bag_begin: int
+    nbags: int
+    pooling: int
+    row_begin: int = 0
+    row_filter: bool = False
+    key_base: int = 0
+    state: Optional[torch.Tensor] = None
+
+    def struct(self) -> L.LookupSegment:
+        w = self.weights
+        es = w.element_size()
+        return L.LookupSegment(
+            weights=w.data_ptr(),
+            out=self.out.data_ptr() + self.out_offset * self.out.element_size(),
+            state=self.state.data_ptr() if self.state is not None else None,
+            ld=w.stride(0),
+            out_ld=self.out_ld,
+            bag_begin=self.bag_begin,
+            row_begin=self.row_begin,
+            key_base=self.key_base,
+            rows=w.shape[0],
+            width=w.shape[1],
+            nbags=self.nbags,
+            pooling=self.pooling,
+            row_filter=1 if self.row_filter else 0,
+            pad_=0,
+        )
+
+
+class SegmentTable:
+    """Device + host copies of a segment list (reusable while buffers live)."""
+
+    def __init__(self, segments: Sequence[Segment], device):
+        self.segments = list(segments)
+        self.n = len(self.segments)
+        self.dev, self.host = device_table(L.LookupSegment, [s.struct() for s in self.segments], device)
+        dts = {s.weights.dtype for s in self.segments}
+        if len(dts) > 1:
+            raise DomainError(f"segments mix dtypes {dts}")
+        self.dtype = dts.pop() if dts else torch.float32
+
+
+def pooled_lookup_fwd(table: SegmentTable, offsets: torch.Tensor, indices: torch.Tensor,
+                      err: Optional[torch.Tensor] = None) -> None:
+    if table.n == 0:
+        return
+    if indices.dtype != torch.int32 or offsets.dtype != torch.int64:
+        raise DomainError("indices must be int32 and offsets int64")
+    L.check(L.lib().dmt_pooled_lookup_fwd(table.dev.data_ptr(), C.addressof(table.host), table.n,
+                                          offsets.data_ptr(), indices.data_ptr(), L.TORCH_DT[table.dtype],
+                                          err.data_ptr() if err is not None else None, L.stream_ptr()),
+            "dmt_pooled_lookup_fwd")
+
+
+def raise_lookup_errors(err: torch.Tensor) -> None:
+    bits = int(err.item())
+    if bits & L.EBIT_BAGLEN:
+        raise TableLookupError("pooling=none requires bags of length 1")
+    if bits & L.EBIT_INDEX:
+        raise TableLookupError("embedding index out of range")
+
+
+def pooled_lookup_bwd_workspace(nnz: int, key_space: int, nsegs: int, device) -> torch.Tensor:
+    n = L.lib().dmt_pooled_lookup_bwd_workspace_size(nnz, key_space, nsegs)
+    return torch.empty(max(1, n), dtype=torch.uint8, device=device)
+
+
+def pooled_lookup_bwd(table: SegmentTable, offsets, indices, nnz: int, key_space: int, optimizer: int,
+                      lr: float, eps: float, workspace: torch.Tensor) -> None:
+    if table.n == 0 or nnz == 0:
+        return
+    L.check(L.lib().dmt_pooled_lookup_bwd(table.dev.data_ptr(), C.addressof(table.host), table.n,
+                                          offsets.data_ptr(), indices.data_ptr(), nnz, key_space,
+                                          L.TORCH_DT[table.dtype], optimizer, lr, eps, workspace.data_ptr(),
+                                          workspace.numel(), L.stream_ptr()),
+            "dmt_pooled_lookup_bwd")
+
+
+# ------------------------------------------------------------ assemble ----
+@dataclass
+class Block:
+    dst_col: int
+    width: int
+    srcs: list  # [(tensor, element offset, ld)]
+
+
+class AssembleTable:
+    def __init__(self, blocks: Sequence[Block], dst: torch.Tensor, rows: int, device):
+        structs, srcs = [], []
+        vec_ok = True
+        es = dst.element_size()
+        vec = 16 // es
+        self.max_width = 0
+        for b in blocks:
+            if b.width == 0:
+                continue
+            structs.append(L.AssembleBlock(dst_col=b.dst_col, width=b.width, nsrc=len(b.srcs),
+                                           first_src=len(srcs), pad_=0))
+            self.max_width = max(self.max_width, b.width)
+            if b.width % vec or b.dst_col % vec:
+                vec_ok = False
+            for t, off, ld in b.srcs:
+                p = t.data_ptr() + off * es
+                srcs.append(L.Src(ptr=p, ld=ld))
+                if p % 16 or ld % vec:
+                    vec_ok = False
+        if dst.data_ptr() % 16 or dst.stride(0) % vec:
+            vec_ok = False
+        self.vec_ok = vec_ok
+        self.n = len(structs)
+        self.rows = rows
+        self.dst = dst
+        self.blocks_dev, self.blocks_host = device_table(L.AssembleBlock, structs, device)
+        self.srcs_dev, self.srcs_host = device_table(L.Src, srcs, device)
+
+    def run(self) -> None:
+        if self.n == 0 or self.rows == 0:
+            return
+        mw = -self.max_width if self.vec_ok else self.max_width
+        L.check(L.lib().dmt_assemble(self.blocks_dev.data_ptr(), self.n, mw, self.srcs_dev.data_ptr(), self.rows,
+                                     self.dst.data_ptr(), self.dst.stride(0), _dt(self.dst), L.stream_ptr()),
+                "dmt_assemble")
+
+
+def assemble(blocks: Sequence[Block], dst: torch.Tensor, rows: int) -> None:
+    AssembleTable(blocks, dst, rows, dst.device).run()
+
+
+class CopyTable:
+    def __init__(self, copies: Sequence[tuple[int, int, int]], device):
+        structs = [L.Copy(src=s, dst=d, bytes=n) for s, d, n in copies if n > 0]
+        self.n = len(structs)
+        self.max_bytes = max((c.bytes for c in structs), default=0)
+        self.dev, self.host = device_table(L.Copy, structs, device)
+
+    def run(self) -> None:
+        if self.n:
+            L.check(L.lib().dmt_batched_copy(self.dev.data_ptr(), self.n, self.max_bytes, L.stream_ptr()),
+                    "dmt_batched_copy")
+
+
+class Copy2DTable:
+    """Batched strided 2-D copies [(src tensor, src elem off, src_ld, dst tensor, dst off, dst_ld, rows, width)]."""
+
+    def __init__(self, copies: Sequence[tuple], device):
+        structs = []
+        self.elem = None
+        self.max_elems = 0
+        for st, so, sld, dt, do, dld, rows, width in copies:
+            if rows * width == 0:
+                continue
+            es = st.element_size()
+            if self.elem is None:
+                self.elem = es
+            elif es != self.elem:
+                raise DomainError("Copy2DTable mixes element sizes")
+            structs.append(L.Copy2D(src=st.data_ptr() + so * es, dst=dt.data_ptr() + do * es, src_ld=sld,
+                                    dst_ld=dld, rows=rows, width=width))
+            self.max_elems = max(self.max_elems, rows * width)
+        self.n = len(structs)
+        self.dev, self.host = device_table(L.Copy2D, structs, device)
+
+    def run(self) -> None:
+        if self.n:
+            L.check(L.lib().dmt_batched_copy2d(self.dev.data_ptr(), self.n, self.elem, self.max_elems,
+                                               L.stream_ptr()), "dmt_batched_copy2d")
+
+
+# ---------------------------------------------------------------- GEMM -----
+def _aligned_operand(x: torch.Tensor) -> torch.Tensor:
+    """TMA needs 16-byte aligned base and row stride: pad K with zeros if not."""
+    es = x.element_size()
+    if x.stride(1) == 1 and x.data_ptr() % 16 == 0 and (x.stride(0) * es) % 16 == 0:
+        return x
+    k = x.shape[1]
+    kp = ((k * es + 15) // 16) * 16 // es
+    y = torch.zeros((x.shape[0], kp), dtype=x.dtype, device=x.device)
+    assemble([Block(0, k, [(x, 0, x.stride(0))])], y, x.shape[0]) if x.stride(1) == 1 else y[:, :k].copy_(x)
+    return y
+
+
+def split_tf32(x: torch.Tensor):
+    x = x.contiguous()
+    hi = torch.empty_like(x)
+    lo = torch.empty_like(x)
+    L.check(L.lib().dmt_split_tf32(x.data_ptr(), hi.data_ptr(), lo.data_ptr(), x.numel(), L.stream_ptr()),
+            "dmt_split_tf32")
+    return hi, lo
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[torch.Tensor] = None,
+         epilogue: int = L.EPI_NONE, x0=None, xl=None, aux=None, beta: float = 0.0,
+         rows_per_group: int = 0, ld_group: int = 0, ld_d: Optional[int] = None,
+         b_split=None) -> torch.Tensor:
+    """out[m, n] = epi(a[m, k] @ b[n, k]^T).  a, b: bf16/f16/f32 (f32 -> 3xTF32).
+
+    ``b_split`` may carry a cached (hi, lo) split of an fp32 weight."""
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[1]:
+        raise ShapeError(f"gemm shapes {tuple(a.shape)} x {tuple(b.shape)}^T")
+    if a.dtype != b.dtype:
+        raise DomainError("gemm operands must share a dtype")
+    m, k = a.shape
+    n = b.shape[0]
+    if m == 0 or n == 0:
+        return out
+    in_dt = _dt(a)
+    if k == 0:
+        raise ShapeError("gemm with k == 0")
+    a_lo = b_lo = None
+    if a.dtype == torch.float32:
+        a_hi, a_lo = split_tf32(_aligned_operand(a))
+        if b_split is not None:
+            b_hi, b_lo = b_split
+        else:
+            b_hi, b_lo = split_tf32(_aligned_operand(b))
+        a, b = a_hi, b_hi
+    else:
+        a = _aligned_operand(a)
+        b = _aligned_operand(b)
+    if bias is not None and (bias.dtype != torch.float32 or not bias.is_contiguous()):
+        bias = bias.float().contiguous()
+    args = L.GemmArgs(
+        a=a.data_ptr(), b=b.data_ptr(), d=out.data_ptr(), bias=L.ptr(bias), x0=L.ptr(x0), xl=L.ptr(xl),
+        aux=L.ptr(aux), m=m, n=n, k=k, lda=a.stride(0), ldb=b.stride(0),
+        ld_d=ld_d if ld_d is not None else out.stride(0),
+        ld_x=(x0.stride(0) if x0 is not None else 0), rows_per_group=rows_per_group, ld_group=ld_group,
+        beta=beta, in_dtype=in_dt, out_dtype=_dt(out), epilogue=epilogue, pad_=0)
+    L.check(L.lib().dmt_gemm_ex(C.byref(args), L.ptr(a_lo), L.ptr(b_lo), L.stream_ptr()), "dmt_gemm")
+    return out
+
+
+def transpose(x: torch.Tensor) -> torch.Tensor:
+    r, c = x.shape
+    out = torch.empty((c, r), dtype=x.dtype, device=x.device)
+    L.check(L.lib().dmt_transpose(x.data_ptr(), r, c, x.stride(0), out.data_ptr(), out.stride(0), _dt(x),
+                                  L.stream_ptr()), "dmt_transpose")
+    return out
+
+
+def column_sum(x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    r, c = x.shape
+    if out is None:
+        out = torch.empty(c, dtype=torch.float32, device=x.device)
+    ws = torch.empty(max(1, L.lib().dmt_column_sum_workspace_size(r, c)), dtype=torch.uint8, device=x.device)
+    L.check(L.lib().dmt_column_sum(x.data_ptr(), r, c, x.stride(0), out.data_ptr(), _dt(x), ws.data_ptr(),
+                                   ws.numel(), L.stream_ptr()), "dmt_column_sum")
+    return out
+
+
+def cross_bwd_pointwise(g, x0, u, gu, dx0) -> None:
+    L.check(L.lib().dmt_cross_bwd_pointwise(g.data_ptr(), x0.data_ptr(), u.data_ptr(), gu.data_ptr(),
+                                            dx0.data_ptr(), g.numel(), _dt(g), L.stream_ptr()),
+            "dmt_cross_bwd_pointwise")
+
+
+def sgd_dense(w: torch.Tensor, g: torch.Tensor, lr: float) -> None:
+    if g.dtype != torch.float32:
+        raise DomainError("dense gradients are fp32")
+    L.check(L.lib().dmt_sgd_dense(w.data_ptr(), g.data_ptr(), w.numel(), lr, _dt(w), L.stream_ptr()),
+            "dmt_sgd_dense")
+
+
+def convert(x: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
+    out = torch.empty(x.shape, dtype=dtype, device=x.device)
+    L.check(L.lib().dmt_convert(x.data_ptr(), _dt(x), out.data_ptr(), _dt(out), x.numel(), L.stream_ptr()),
+            "dmt_convert")
+    return out

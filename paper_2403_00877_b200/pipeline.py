@@ -1,0 +1,366 @@
+"""Device pipeline of the SPTT forward/backward and the flat baseline.
+
+One engine instance serves the ranks hosted by this process: every rank on a
+single GPU (LoopbackFabric, used by the reference-API drop-in and the parity
+tests) or exactly one rank per GPU (NcclFabric, the distributed training
+path).  Both run the same phases in the same order:
+
+  forward  a  bucketize (dmt_kjt_bucketize) + all-to-all(v) of lengths/values
+           b  offsets scan + pooled lookup straight into the step-d send buffer
+              (class-order permute and stacking fused: dmt_pooled_lookup_fwd)
+           d  tower all-to-all(v)                          (SPTT)   | c  world all-to-all (flat)
+           e  assemble / regroup (dmt_assemble) + tower module GEMMs (dmt_gemm)
+           f  per-class all-to-all, then output gather (dmt_assemble)
+  backward f^-1 pack + class all-to-all, TM backward + tower all-reduce of the
+           TM weight grads, d^-1 pack + tower all-to-all, then the fused
+           sort/segment-reduce/optimizer embedding update (dmt_pooled_lookup_bwd)
+           on the owner (no a^-1 exchange: the owner already holds the indices).
+
+Reference: towersim/exchange.py:149-462 (forward only; the backward is new).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _lib as L
+from . import kernels as K
+from .embedding import POOL_MEAN, ROW_WISE, ShardedEmbedding
+from .errors import DomainError
+from .fabric import Fabric
+from .plan import ExchangePlan
+from .simnet import CommTrace
+
+
+@dataclass
+class KJT:
+    """A rank's keyed jagged tensor, keys (features) major.
+
+    lengths (F*B,) int32 and values (nnz,) int32 on the device; the host keeps
+    the per-feature nnz (as TorchRec's length_per_key) so the step-a value
+    splits need no device sync when every rank knows its own counts."""
+
+    lengths: torch.Tensor
+    values: torch.Tensor
+    nnz_per_feature: list
+    B: int
+    offsets: Optional[torch.Tensor] = None
+
+    @property
+    def F(self) -> int:
+        return len(self.nnz_per_feature)
+
+    def ensure_offsets(self) -> torch.Tensor:
+        if self.offsets is None:
+            self.offsets = K.lengths_to_offsets(self.lengths)
+        return self.offsets
+
+
+class SpttEngine:
+    def __init__(self, plan: ExchangePlan, placement: ShardedEmbedding, fabric: Fabric, dtype: torch.dtype,
+                 device=None, tower_modules: Optional[dict] = None, mode: str = "sptt",
+                 trace: Optional[CommTrace] = None, rowwise_reducescatter: bool = False):
+        if mode not in ("sptt", "flat"):
+            raise DomainError(f"unknown mode {mode!r}")
+        if mode == "sptt" and plan.feature_towers is None:
+            raise DomainError("SPTT mode needs feature_towers")
+        self.plan, self.placement, self.fabric = plan, placement, fabric
+        self.dtype = dtype
+        self.es = torch.empty((), dtype=dtype).element_size()
+        self.device = device or torch.device("cuda")
+        self.tm = tower_modules or {}
+        self.mode = mode
+        self.trace = trace
+        self.rs = rowwise_reducescatter
+        self.local = list(fabric.local_ranks)
+        p = plan
+        dev = self.device
+        self.weights = {sid: placement.device_shard(sid, dtype, dev) for r in self.local for sid in p.by_owner[r]}
+        self.state = {}
+        self.slot_feature = torch.tensor(p.a_slot_feature or [0], dtype=torch.int32, device=dev)
+        # persistent buffers + descriptor tables (built once; pointers stay valid)
+        self.buf = {}
+        self.seg_fwd, self.seg_bwd = {}, {}
+        self.asm_e, self.asm_out, self.asm_c = {}, {}, {}
+        sptt = mode == "sptt"
+        for r in self.local:
+            nsend = p.send_d_size(r) if sptt else p.send_c_size(r)
+            b = {"send_x": torch.empty(max(1, nsend), dtype=dtype, device=dev),
+                 "grad_x": torch.empty(max(1, nsend), dtype=dtype, device=dev)}
+            if sptt:
+                b["recv_d"] = torch.empty(max(1, sum(p.d_recv_splits(r))), dtype=dtype, device=dev)
+                b["X"] = torch.empty((p.T * p.B, p.x_width(r)), dtype=dtype, device=dev)
+                t = p.tower_of(r)
+                if t not in self.tm and p.O[t] == p.x_width(r):
+                    b["Y"] = b["X"]  # pass-through tower: X is the step-f send buffer
+                else:
+                    b["Y"] = torch.zeros((p.T * p.B, p.O[t]), dtype=dtype, device=dev)
+                b["recv_f"] = torch.empty(max(1, sum(p.f_recv_splits(r))), dtype=dtype, device=dev)
+                b["out"] = torch.empty((p.B, p.out_width()), dtype=dtype, device=dev)
+            else:
+                b["recv_c"] = torch.empty(max(1, sum(p.c_recv_splits(r))), dtype=dtype, device=dev)
+                b["out"] = torch.empty((p.B, p.flat_width()), dtype=dtype, device=dev)
+            self.buf[r] = b
+            self.seg_fwd[r] = self._segments(r, b["send_x"])
+            self.seg_bwd[r] = self._segments(r, b["grad_x"], with_keys=True)
+            if sptt:
+                self.asm_e[r] = self._assemble_table(p.e_blocks(r), b["recv_d"], b["X"], p.T * p.B)
+                blocks = [K.Block(col, w, [(b["recv_f"], off, w)]) for col, w, off in p.out_blocks_tower()]
+                self.asm_out[r] = K.AssembleTable(blocks, b["out"], p.B, dev)
+            else:
+                self.asm_c[r] = self._assemble_table(p.c_blocks(), b["recv_c"], b["out"], p.B)
+        self._bwd_ws = {}
+
+    # ----------------------------------------------------------- tables ----
+    def _segments(self, r: int, out: torch.Tensor, with_keys: bool = False) -> K.SegmentTable:
+        p = self.plan
+        segs = []
+        key_base, kb = {}, 0
+        for sid in p.by_owner[r]:
+            key_base[sid] = kb
+            kb += self.placement.shards[sid].rows
+        self.key_space = getattr(self, "key_space", {})
+        self.key_space[r] = kb
+        for (pp, k, off, w) in p.lookup_out_offsets(r, self.mode == "sptt"):
+            sid = p.by_owner[r][k]
+            sh = self.placement.shards[sid]
+            pool = p.pooling[sh.table_id]
+            code = L.POOL_SUM if sh.scheme == ROW_WISE else L.POOL_CODE[pool]
+            if sh.scheme == ROW_WISE and pool == POOL_MEAN:
+                raise DomainError("mean pooling over row-wise shards is not defined (partials sum)")
+            segs.append(K.Segment(weights=self.weights[sid], out=out, out_offset=off, out_ld=w,
+                                  bag_begin=(pp * p.S[r] + k) * p.B, nbags=p.B, pooling=code,
+                                  row_begin=sh.row_range[0], row_filter=sh.scheme == ROW_WISE,
+                                  key_base=key_base[sid], state=self.state.get(sid)))
+        return K.SegmentTable(segs, self.device)
+
+    def _assemble_table(self, fblocks, src: torch.Tensor, dst: torch.Tensor, rows: int) -> K.AssembleTable:
+        blocks = []
+        for fb in fblocks:
+            if fb.rowwise:
+                blocks.append(K.Block(fb.dst_col, fb.width, [(src, pc.offset, pc.ld) for pc in fb.pieces]))
+            else:
+                for pc in fb.pieces:
+                    blocks.append(K.Block(fb.dst_col + pc.c0, pc.width, [(src, pc.offset, pc.ld)]))
+        return K.AssembleTable(blocks, dst, rows, self.device)
+
+    def enable_adagrad(self) -> None:
+        """Allocate row-wise Adagrad accumulators (one fp32 per row) and
+        rebuild the backward segment tables to point at them."""
+        for r in self.local:
+            for sid in self.plan.by_owner[r]:
+                if sid not in self.state:
+                    self.state[sid] = torch.zeros(self.placement.shards[sid].rows, dtype=torch.float32,
+                                                  device=self.device)
+            self.seg_bwd[r] = self._segments(r, self.buf[r]["grad_x"], with_keys=True)
+
+    # ---------------------------------------------------------- forward ----
+    def forward(self, kjts: dict, save: bool = False, check_indices: bool = False) -> dict:
+        p, fab, dev = self.plan, self.fabric, self.device
+        world = list(range(p.G))
+        # step a: bucketize per src, exchange lengths then values
+        send_len, send_val, len_splits, val_splits = {}, {}, {}, {}
+        for r in self.local:
+            kj = kjts[r]
+            if kj.B != p.B or kj.F != len(p.features):
+                raise DomainError("KJT shape does not match the plan")
+            offs = kj.ensure_offsets()
+            slot_offs = p.a_slot_value_offsets(kj.nnz_per_feature)
+            total = slot_offs[-1]
+            send_len[r] = torch.empty(max(1, len(p.a_slots) * p.B), dtype=torch.int32, device=dev)
+            send_val[r] = torch.empty(max(1, total), dtype=torch.int32, device=dev)
+            if p.a_slots:
+                so = torch.tensor(slot_offs, dtype=torch.int64).to(dev, non_blocking=True)
+                K.kjt_bucketize(kj.lengths, offs, kj.values, p.B, self.slot_feature, so, send_len[r], send_val[r])
+            len_splits[r] = p.a_send_length_splits()
+            val_splits[r] = p.a_send_value_splits(kj.nnz_per_feature)
+        recv_val_splits = fab.exchange_counts(world, val_splits)
+        recv_len, recv_val = {}, {}
+        for r in self.local:
+            recv_len[r] = torch.empty(max(1, p.owner_bags(r)), dtype=torch.int32, device=dev)
+            recv_val[r] = torch.empty(max(1, sum(recv_val_splits[r])), dtype=torch.int32, device=dev)
+        fab.alltoallv(world, "a_len", send_len, len_splits, recv_len,
+                      {r: [p.S[r] * p.B] * p.G for r in self.local})
+        fab.alltoallv(world, "a", send_val, val_splits, recv_val, recv_val_splits, self.trace, 4)
+        # step b: lookup (+ fused permute) on every owner
+        self._owner = {}
+        err = torch.zeros(1, dtype=torch.int32, device=dev) if check_indices else None
+        for r in self.local:
+            offsets = K.lengths_to_offsets(recv_len[r][: p.owner_bags(r)])
+            K.pooled_lookup_fwd(self.seg_fwd[r], offsets, recv_val[r], err)
+            self._owner[r] = (offsets, recv_val[r], sum(recv_val_splits[r]))
+        if err is not None:
+            K.raise_lookup_errors(err)
+        if self.mode == "flat":
+            return self._flat_forward()
+        # step d: tower all-to-alls
+        send = {r: self.buf[r]["send_x"] for r in self.local}
+        recv = {r: self.buf[r]["recv_d"] for r in self.local}
+        for g in self._groups(p.group_of):
+            self._trace_d(g)
+            fab.alltoallv(g, "d", send, {r: p.d_send_splits(r) for r in g}, recv,
+                          {r: p.d_recv_splits(r) for r in g}, None)
+        # step e: regroup + tower module
+        for r in self.local:
+            self.asm_e[r].run()
+            t = p.tower_of(r)
+            if t in self.tm:
+                self.tm[t].forward(self.buf[r]["X"], save=save, out=self.buf[r]["Y"])
+                if save:
+                    self.buf[r]["tm_saved"] = self.tm[t]._saved
+        # step f: per-class all-to-alls, then tower-grouped output
+        send = {r: self.buf[r]["Y"].view(-1) for r in self.local}
+        recv = {r: self.buf[r]["recv_f"] for r in self.local}
+        for g in self._groups(p.class_group_of):
+            fab.alltoallv(g, "f", send, {r: p.f_send_splits(r) for r in g}, recv,
+                          {r: p.f_recv_splits(r) for r in g}, self.trace, self.es)
+        out = {}
+        for r in self.local:
+            self.asm_out[r].run()
+            out[r] = self.buf[r]["out"]
+        return out
+
+    def _flat_forward(self) -> dict:
+        p, fab = self.plan, self.fabric
+        world = list(range(p.G))
+        send = {r: self.buf[r]["send_x"] for r in self.local}
+        recv = {r: self.buf[r]["recv_c"] for r in self.local}
+        fab.alltoallv(world, "c", send, {r: p.c_send_splits(r) for r in world}, recv,
+                      {r: p.c_recv_splits(r) for r in world}, self.trace, self.es)
+        out = {}
+        for r in self.local:
+            self.asm_c[r].run()
+            out[r] = self.buf[r]["out"]
+        return out
+
+    def _groups(self, group_fn) -> list:
+        seen, out = set(), []
+        for r in self.local:
+            g = tuple(group_fn(r))
+            if g not in seen:
+                seen.add(g)
+                out.append(list(g))
+        return out
+
+    def _trace_d(self, group) -> None:
+        """Step-d byte accounting exactly as the reference records it
+        (exchange.py:367-395), including the reduce-scatter form."""
+        if self.trace is None:
+            return
+        p = self.plan
+        rs_tables = set()
+        if self.rs:
+            rs_tables = {f for f in p.features
+                         if any(s.scheme == ROW_WISE for s in self.placement.shards if s.table_id == f)}
+        tower = p.tower_of(group[0])
+        for owner in group:
+            for member in group:
+                if owner not in self.fabric.local_ranks and member not in self.fabric.local_ranks:
+                    continue
+                if owner not in self.fabric.local_ranks:
+                    continue
+                n = sum(p.T * p.B * self.placement.shards[sid].width for sid in p.by_owner[owner]
+                        if self.placement.shards[sid].table_id not in rs_tables)
+                self.trace.record_elements("d", owner, member, n, self.es)
+        for f in p.tower_features[tower]:
+            if f not in rs_tables:
+                continue
+            contributors = sorted({self.placement.shards[sid].rank for sid in p.live
+                                   if self.placement.shards[sid].table_id == f})
+            for dst in group:
+                for src in group:
+                    if src in contributors and src in self.fabric.local_ranks:
+                        self.trace.record_elements("d", src, dst, p.T * p.B * p.dims[f], self.es)
+
+    # --------------------------------------------------------- backward ----
+    def backward(self, grad_out: dict, lr: float, optimizer: int = L.OPT_SGD, eps: float = 1e-8,
+                 tm_lr: Optional[float] = None) -> None:
+        """Backward of the last forward(save=True) + fused optimizer updates."""
+        p, fab, dev = self.plan, self.fabric, self.device
+        if self.mode == "flat":
+            return self._flat_backward(grad_out, lr, optimizer, eps)
+        # f^-1: pack the tower-grouped gradient into per-tower blocks (the step-f
+        # receive layout), send each block back to the member that produced it
+        gsend, grecv = {}, {}
+        for r in self.local:
+            gf = torch.empty_like(self.buf[r]["recv_f"])
+            copies = []
+            col, off = 0, 0
+            ow = p.out_width()
+            for t in range(p.T):
+                copies.append((grad_out[r], col, ow, gf, off, p.O[t], p.B, p.O[t]))
+                col += p.O[t]
+                off += p.B * p.O[t]
+            K.Copy2DTable(copies, dev).run()
+            gsend[r] = gf
+            grecv[r] = torch.empty((p.T * p.B, p.O[p.tower_of(r)]), dtype=self.dtype, device=dev)
+        for g in self._groups(p.class_group_of):
+            fab.alltoallv(g, "f_bwd", gsend, {r: p.f_recv_splits(r) for r in g}, {r: grecv[r].view(-1) for r in self.local},
+                          {r: p.f_send_splits(r) for r in g})
+        # e^-1: tower module backward (weight grads summed over the tower)
+        dX = {}
+        tower_grads = {}
+        for r in self.local:
+            t = p.tower_of(r)
+            if t in self.tm:
+                self.tm[t]._saved = self.buf[r]["tm_saved"]
+                dX[r] = self.tm[t].backward(grecv[r])
+                acc = tower_grads.setdefault(t, {})
+                for k, v in self.tm[t].grads.items():
+                    acc[k] = v.clone() if k not in acc else acc[k].add_(v)
+            else:
+                dX[r] = grecv[r]
+        for t, grads in tower_grads.items():
+            group = p.layout.tower_ranks(t, p.topo)
+            fab.all_reduce_(group, grads)
+            self.tm[t].grads = grads
+            self.tm[t].sgd_step(tm_lr if tm_lr is not None else lr)
+        # d^-1: scatter dX columns back into the step-d receive layout
+        dsend, drecv = {}, {}
+        for r in self.local:
+            gd = torch.empty_like(self.buf[r]["recv_d"])
+            copies = []
+            xw = p.x_width(r)
+            for fb in p.e_blocks(r):
+                for pc in fb.pieces:
+                    copies.append((dX[r], fb.dst_col + pc.c0, xw, gd, pc.offset, pc.ld, p.T * p.B, pc.width))
+            K.Copy2DTable(copies, dev).run()
+            dsend[r] = gd
+            drecv[r] = self.buf[r]["grad_x"]
+        for g in self._groups(p.group_of):
+            fab.alltoallv(g, "d_bwd", dsend, {r: p.d_recv_splits(r) for r in g}, drecv,
+                          {r: p.d_send_splits(r) for r in g})
+        self._embedding_update(lr, optimizer, eps)
+
+    def _flat_backward(self, grad_out, lr, optimizer, eps):
+        p, fab, dev = self.plan, self.fabric, self.device
+        world = list(range(p.G))
+        gsend = {}
+        fw = p.flat_width()
+        for r in self.local:
+            gc = torch.empty_like(self.buf[r]["recv_c"])
+            copies = []
+            for fb in p.c_blocks():
+                for pc in fb.pieces:
+                    copies.append((grad_out[r], fb.dst_col + pc.c0, fw, gc, pc.offset, pc.ld, p.B, pc.width))
+            K.Copy2DTable(copies, dev).run()
+            gsend[r] = gc
+        fab.alltoallv(world, "c_bwd", gsend, {r: p.c_recv_splits(r) for r in world},
+                      {r: self.buf[r]["grad_x"] for r in self.local}, {r: p.c_send_splits(r) for r in world})
+        self._embedding_update(lr, optimizer, eps)
+
+    def _embedding_update(self, lr, optimizer, eps):
+        if optimizer == L.OPT_ROWWISE_ADAGRAD and not self.state:
+            self.enable_adagrad()
+        for r in self.local:
+            offsets, vals, nnz = self._owner[r]
+            ks = self.key_space[r]
+            need = L.lib().dmt_pooled_lookup_bwd_workspace_size(nnz, ks, self.seg_bwd[r].n)
+            ws = self._bwd_ws.get(r)
+            if ws is None or ws.numel() < need:
+                ws = torch.empty(max(1, need), dtype=torch.uint8, device=self.device)
+                self._bwd_ws[r] = ws
+            K.pooled_lookup_bwd(self.seg_bwd[r], offsets, vals, nnz, ks, optimizer, lr, eps, ws)

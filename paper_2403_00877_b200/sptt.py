@@ -1,0 +1,156 @@
+"""SPTT training module: the distributed forward/backward + optimizer step of
+the DMT embedding path (e).
+
+One process per GPU (NcclFabric) or every rank on one GPU (LoopbackFabric).
+A step is: step a-f forward (towersim/exchange.py:275-462 semantics), tower
+modules on each tower's data-parallel ranks, the reverse exchange, TM weight
+gradients all-reduced inside the tower and a fused
+sort/segment-reduce/SGD-or-row-wise-Adagrad update of every embedding shard on
+its owner.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .embedding import EmbeddingTable, ShardedEmbedding, TablePlan, shard_tables
+from .fabric import Fabric, LoopbackFabric
+from .pipeline import KJT, SpttEngine
+from .plan import ExchangePlan
+from .topology import ClusterTopology, TowerLayout
+from .towermod import PASSTHROUGH, TMConfig, TowerModule, init_tm_weights, tm_output_width
+
+
+class SPTT:
+    def __init__(self, topo: ClusterTopology, layout: TowerLayout, placement: ShardedEmbedding,
+                 feature_towers: dict, pooling: dict, local_batch: int, fabric: Fabric,
+                 tm: Optional[object] = None, dtype: torch.dtype = torch.float32, device=None,
+                 mode: str = "sptt", lr: float = 0.01, optimizer: str = "sgd", eps: float = 1e-8,
+                 trace=None):
+        self.topo, self.layout, self.placement = topo, layout, placement
+        self.device = device or torch.device("cuda")
+        feats = sorted(pooling)
+        dims = {f: placement.tables[f].dim for f in feats}
+        T = layout.num_towers
+        by_tower = {t: [f for f in feats if feature_towers[f] == t] for t in range(T)}
+        widths, tms = {}, {}
+        self.tm_cfg = {}
+        for t in range(T):
+            cfg = tm.get(t) if isinstance(tm, dict) else tm
+            cfg = cfg or TMConfig(kind=PASSTHROUGH)
+            self.tm_cfg[t] = cfg
+            if cfg.kind != PASSTHROUGH and mode == "sptt":
+                n = dims[by_tower[t][0]] if by_tower[t] else 1
+                widths[t] = tm_output_width(cfg, len(by_tower[t]), n)
+                local_towers = {r // layout.group_width(topo) for r in fabric.local_ranks}
+                if by_tower[t] and t in local_towers:
+                    tms[t] = TowerModule(cfg, len(by_tower[t]), n, init_tm_weights(cfg, len(by_tower[t]), n, salt=t),
+                                         dtype=dtype, device=self.device)
+        self.plan = ExchangePlan(topo, layout, placement.shards, feats, dims, pooling, local_batch,
+                                 feature_towers=feature_towers if mode == "sptt" else None, tower_widths=widths)
+        self.engine = SpttEngine(self.plan, placement, fabric, dtype, self.device, tower_modules=tms, mode=mode,
+                                 trace=trace)
+        self.tms = tms
+        self.lr, self.eps = lr, eps
+        self.opt = L.OPT_ROWWISE_ADAGRAD if optimizer == "adagrad" else L.OPT_SGD
+        if self.opt == L.OPT_ROWWISE_ADAGRAD:
+            self.engine.enable_adagrad()
+
+    def forward(self, kjts: dict, save: bool = True) -> dict:
+        return self.engine.forward(kjts, save=save)
+
+    def backward(self, grads: dict) -> None:
+        self.engine.backward(grads, self.lr, self.opt, self.eps)
+
+    def train_step(self, kjts: dict, grads: dict) -> dict:
+        outs = self.forward(kjts, save=True)
+        self.backward(grads)
+        return outs
+
+
+def build_world(G_hosts: int, ranks_per_host: int, hosts_per_tower: int, num_tables: int, rows: int, dim: int,
+                seed: int = 0, dtype=np.float32, scheme: str = "table_wise", shards_per_table: int = 1,
+                assignment: Optional[dict] = None):
+    """Synthetic world: uniform(-1, 1) tables (embedding.py:58-60 generator),
+    contiguous balanced feature->tower assignment, round-robin placement."""
+    topo = ClusterTopology(G_hosts, ranks_per_host)
+    W = ranks_per_host * hosts_per_tower
+    layout = TowerLayout(topo.world_size // W, hosts_per_tower)
+    T = layout.num_towers
+    tables = {}
+    for t in range(num_tables):
+        vals = np.random.default_rng([seed, t]).uniform(-1.0, 1.0, size=(rows, dim)).astype(dtype)
+        tables[t] = EmbeddingTable(t, rows, dim, vals)
+    if assignment is None:
+        base, extra = divmod(num_tables, T)
+        assignment, f = {}, 0
+        for t in range(T):
+            for _ in range(base + (1 if t < extra else 0)):
+                assignment[f] = t
+                f += 1
+    plan = {t: TablePlan(scheme, 1 if scheme == "table_wise" else shards_per_table, assignment[t]) for t in tables}
+    return topo, layout, shard_tables(tables, plan, topo, layout), assignment
+
+
+def random_kjt(F: int, B: int, rows: int, L_: int, gen: torch.Generator, device) -> KJT:
+    """Fixed pooling factor L (C2/C3: L = 20), uniform indices (embedding.py:290)."""
+    lengths = torch.full((F * B,), L_, dtype=torch.int32, device=device)
+    values = torch.randint(0, rows, (F * B * L_,), generator=gen, device=device, dtype=torch.int32)
+    return KJT(lengths=lengths, values=values, nnz_per_feature=[B * L_] * F, B=B)
+
+
+def smoke_train_step() -> None:
+    """One loopback SPTT train step (2 towers x 2 ranks, DLRM TM, fp32) checked
+    against the oracle's flat-model restatement (used by __graft_entry__.smoke)."""
+    import oracle
+
+    dev = torch.device("cuda")
+    topo, layout, placement, assignment = build_world(2, 2, 1, 6, 40, 16, seed=5)
+    G, B, F = 4, 3, 6
+    pooling = {f: "sum" for f in range(F)}
+    cfg = TMConfig(kind="dlrm", out_dim=8, per_feature_outputs=1, flat_outputs=1, seed=1)
+    before = {t: placement.tables[t].values.astype(np.float64).copy() for t in range(F)}
+    model = SPTT(topo, layout, placement, assignment, pooling, B, LoopbackFabric(G, dev), tm=cfg,
+                 dtype=torch.float32, lr=0.1)
+    rng = np.random.default_rng(9)
+    lens = rng.integers(0, 4, size=(G, F, B)).astype(np.int32)
+    vals = rng.integers(0, 40, size=int(lens.sum())).astype(np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens.reshape(-1))])
+    kjts = {}
+    for r in range(G):
+        seg = vals[offs[r * F * B]:offs[(r + 1) * F * B]]
+        kjts[r] = KJT(torch.from_numpy(lens[r].reshape(-1)).to(dev), torch.from_numpy(seg.astype(np.int32)).to(dev),
+                      [int(lens[r, f].sum()) for f in range(F)], B)
+    O = model.plan.out_width()
+    grads = {r: torch.from_numpy(rng.normal(size=(B, O)).astype(np.float32)).to(dev) for r in range(G)}
+    outs = model.train_step(kjts, grads)
+    torch.cuda.synchronize()
+    # oracle: pooled per rank -> TM per tower -> grads -> table SGD
+    shards = [(s.table_id, s.rank, s.scheme, s.row_range, s.col_range) for s in placement.shards]
+    flat, _, _, _ = oracle.baseline_forward(lens, vals, list(range(F)), pooling, before, shards, oracle.OTopo(2, 2))
+    ocfg = {"kind": "dlrm", "out_dim": 8, "per_feature_outputs": 1, "flat_outputs": 1, "cross_layers": 3, "seed": 1}
+    tw = {t: oracle.init_tm_weights(ocfg, 3, 16, salt=t) for t in range(2)}
+    expect_tables = {t: before[t].copy() for t in range(F)}
+    for r in range(G):
+        g_r = grads[r].double().cpu().numpy()
+        col = 0
+        for t in range(2):
+            fs = [f for f in range(F) if assignment[f] == t]
+            x = flat[r][:, fs[0] * 16:(fs[-1] + 1) * 16].reshape(B, len(fs), 16)
+            ow = oracle.tm_output_width(ocfg, len(fs), 16)
+            y = oracle.tm_forward(x, ocfg, tw[t])
+            assert np.allclose(outs[r][:, col:col + ow].double().cpu().numpy(), y, rtol=1e-5, atol=1e-5)
+            dx, _ = oracle.tm_backward(x, ocfg, tw[t], g_r[:, col:col + ow])
+            col += ow
+            for i, f in enumerate(fs):
+                base = (r * F + f) * B
+                for b in range(B):
+                    for k in range(offs[base + b], offs[base + b + 1]):
+                        expect_tables[f][vals[k]] -= 0.1 * dx[b, i]
+    for sid, sh in enumerate(placement.shards):
+        got = model.engine.weights[sid].double().cpu().numpy()
+        np.testing.assert_allclose(got, expect_tables[sh.table_id], rtol=1e-4, atol=1e-5)

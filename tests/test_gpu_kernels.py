@@ -1,0 +1,194 @@
+"""GPU parity of the individual libdmt kernels against the CPU oracle / golden
+fixtures (bit-exact for integer and routing work, toleranced for float GEMMs)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_meta, golden_npz
+
+pytestmark = pytest.mark.gpu
+
+from oracle import bf16_round, pool, route_step_a  # noqa: E402
+
+
+def dev():
+    return torch.device("cuda")
+
+
+def test_lengths_to_offsets_matches_cumsum():
+    from paper_2403_00877_b200 import kernels as K
+
+    rng = np.random.default_rng(0)
+    for n in (0, 1, 7, 1023, 8192, 8193, 212_992, 1_000_003):
+        lens = rng.integers(0, 40, size=n).astype(np.int32)
+        got = K.lengths_to_offsets(torch.from_numpy(lens).to(dev())).cpu().numpy()
+        want = np.concatenate([[0], np.cumsum(lens, dtype=np.int64)])
+        assert np.array_equal(got, want), n
+
+
+def test_bucketize_matches_golden_step_a():
+    from paper_2403_00877_b200 import kernels as K
+
+    m = golden_meta()["worked_2x4"]
+    arr = golden_npz("worked_2x4")
+    shards = [(a, b, c, tuple(d), tuple(e)) for a, b, c, d, e in m["placement"]]
+    G, F, B = arr["lengths"].shape
+    routed = route_step_a(arr["lengths"], arr["values"], list(range(F)), shards, G)
+    offs_all = np.concatenate([[0], np.cumsum(arr["lengths"].reshape(-1))])
+    slots = [(o, sid) for o in range(G) for sid, s in enumerate(shards) if s[1] == o]
+    slot_feature = [shards[sid][0] for _, sid in slots]
+    for src in range(G):
+        lens = arr["lengths"][src].reshape(-1).astype(np.int32)
+        vals = arr["values"][offs_all[src * F * B]:offs_all[(src + 1) * F * B]].astype(np.int32)
+        nnz = [int(lens[f * B:(f + 1) * B].sum()) for f in range(F)]
+        slot_off = np.concatenate([[0], np.cumsum([nnz[f] for f in slot_feature])]).astype(np.int64)
+        L = torch.from_numpy(lens).to(dev())
+        O = K.lengths_to_offsets(L)
+        V = torch.from_numpy(vals).to(dev())
+        out_len = torch.empty(len(slots) * B, dtype=torch.int32, device=dev())
+        out_val = torch.empty(max(1, int(slot_off[-1])), dtype=torch.int32, device=dev())
+        K.kjt_bucketize(L, O, V, B, torch.tensor(slot_feature, dtype=torch.int32, device=dev()),
+                        torch.from_numpy(slot_off).to(dev()), out_len, out_val)
+        ol, ov = out_len.cpu().numpy(), out_val.cpu().numpy()
+        for s, (owner, sid) in enumerate(slots):
+            bundle = {x[0]: x for x in routed[(src, owner)]}
+            _, want_len, want_idx = bundle[sid]
+            assert np.array_equal(ol[s * B:(s + 1) * B], want_len)
+            assert np.array_equal(ov[slot_off[s]:slot_off[s + 1]], want_idx)
+
+
+def _lookup_gpu(table, lens, idx, mode, out_dtype=None, row_begin=0, row_filter=False):
+    from paper_2403_00877_b200 import _lib as L
+    from paper_2403_00877_b200 import kernels as K
+
+    w = table if isinstance(table, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(table)).to(dev())
+    n = len(lens)
+    out = torch.zeros((n, w.shape[1]), dtype=w.dtype, device=dev())
+    L_ = torch.from_numpy(np.asarray(lens, dtype=np.int32)).to(dev())
+    offs = K.lengths_to_offsets(L_)
+    I = torch.from_numpy(np.asarray(idx, dtype=np.int32)).to(dev())
+    seg = K.Segment(weights=w, out=out, out_offset=0, out_ld=w.shape[1], bag_begin=0, nbags=n,
+                    pooling=L.POOL_CODE[mode], row_begin=row_begin, row_filter=row_filter)
+    err = torch.zeros(1, dtype=torch.int32, device=dev())
+    K.pooled_lookup_fwd(K.SegmentTable([seg], dev()), offs, I, err)
+    return out, int(err.item())
+
+
+def test_lookup_golden_long_bags_bit_exact():
+    g = golden_npz("lookup_order")
+    lens = np.diff(g["offsets"])
+    out, err = _lookup_gpu(g["table"], lens, g["values"], "sum")
+    assert err == 0
+    assert np.array_equal(out.double().cpu().numpy(), g["out"])
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("width", [1, 3, 8, 16, 64, 128, 200, 256, 512])
+@pytest.mark.parametrize("mode", ["sum", "mean", "none"])
+def test_lookup_widths_modes_bit_exact(dtype, width, mode):
+    rng = np.random.default_rng(width)
+    rows = 777
+    table = rng.uniform(-1, 1, (rows, width)).astype(dtype)
+    n = 300
+    lens = np.ones(n, np.int64) if mode == "none" else rng.integers(0, 33, size=n)
+    idx = rng.integers(0, rows, size=int(lens.sum()))
+    out, err = _lookup_gpu(table, lens, idx, mode)
+    assert err == 0
+    want = pool(table, lens, idx, mode)
+    assert np.array_equal(out.double().cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("width", [8, 64, 128, 256])
+def test_lookup_bf16_matches_fp32_accumulate_then_round(width):
+    rng = np.random.default_rng(3)
+    rows = 1000
+    t32 = bf16_round(rng.uniform(-1, 1, (rows, width)).astype(np.float32))
+    lens = rng.integers(0, 40, size=200)
+    idx = rng.integers(0, rows, size=int(lens.sum()))
+    w = torch.from_numpy(t32).to(dev()).to(torch.bfloat16)
+    out, err = _lookup_gpu(w, lens, idx, "sum")
+    want = bf16_round(pool(t32, lens, idx, "sum").astype(np.float32))
+    assert np.array_equal(out.float().cpu().numpy(), want)
+
+
+def test_lookup_row_filter_and_errors():
+    rng = np.random.default_rng(5)
+    table = rng.uniform(-1, 1, (100, 16)).astype(np.float32)
+    lens = rng.integers(0, 10, size=50)
+    idx = rng.integers(0, 100, size=int(lens.sum()))
+    shard = torch.from_numpy(table[40:70]).to(dev())
+    out, err = _lookup_gpu(shard, lens, idx, "sum", row_begin=40, row_filter=True)
+    assert err == 0
+    keep = (idx >= 40) & (idx < 70)
+    bag = np.repeat(np.arange(50), lens)
+    nl = np.bincount(bag[keep], minlength=50)
+    want = pool(table[40:70], nl, idx[keep] - 40, "sum")
+    assert np.array_equal(out.double().cpu().numpy(), want)
+    # out-of-range index on a non-filtered shard / bad bag length flag errors
+    _, err = _lookup_gpu(table, [2], [0, 100], "sum")
+    assert err & 1
+    _, err = _lookup_gpu(table, [2], [0, 1], "none")
+    assert err & 2
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 64, 64), (300, 100, 72), (1000, 256, 128), (4096, 512, 1024),
+                                   (7, 5, 8), (129, 257, 200)])
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
+def test_gemm_bias_vs_torch(m, n, k, dt):
+    from paper_2403_00877_b200 import _lib as L
+    from paper_2403_00877_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n)
+    a = torch.randn(m, k, device="cuda", generator=g).to(dt)
+    b = torch.randn(n, k, device="cuda", generator=g).to(dt)
+    bias = torch.randn(n, device="cuda", generator=g)
+    out = torch.empty(m, n, device="cuda", dtype=torch.float32)
+    K.gemm(a, b, out, bias=bias, epilogue=L.EPI_BIAS)
+    want = a.double() @ b.double().T + bias.double()
+    tol = 1e-5 if dt == torch.float32 else 1e-2
+    scale = (a.double().abs() @ b.double().abs().T).max().item()
+    err = (out.double() - want).abs().max().item()
+    assert err <= tol * scale, (err, scale)
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
+def test_gemm_cross_epilogue_vs_torch(dt):
+    from paper_2403_00877_b200 import _lib as L
+    from paper_2403_00877_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    m, M = 513, 192
+    x0 = torch.randn(m, M, device="cuda", generator=g).to(dt)
+    xl = torch.randn(m, M, device="cuda", generator=g).to(dt)
+    w = (torch.randn(M, M, device="cuda", generator=g) / M ** 0.5).to(dt)
+    b = torch.randn(M, device="cuda", generator=g)
+    out = torch.empty(m, M, device="cuda", dtype=dt)
+    u = torch.empty(m, M, device="cuda", dtype=dt)
+    K.gemm(xl, w, out, bias=b, epilogue=L.EPI_CROSS, x0=x0, xl=xl, aux=u)
+    uu = xl.double() @ w.double().T + b.double()
+    want = x0.double() * uu + xl.double()
+    tol = 1e-5 if dt == torch.float32 else 2e-2
+    assert (u.double() - uu).abs().max().item() <= tol * max(1.0, uu.abs().max().item())
+    assert (out.double() - want).abs().max().item() <= tol * max(1.0, want.abs().max().item())
+
+
+def test_gemm_grouped_rows_output():
+    """DLRM per-feature projection written straight into the tower output."""
+    from paper_2403_00877_b200 import _lib as L
+    from paper_2403_00877_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(2)
+    rows, F, N, cD, pD = 70, 5, 32, 16, 8
+    O = pD + F * cD
+    x = torch.randn(rows, F * N, device="cuda", generator=g)
+    w = torch.randn(cD, N, device="cuda", generator=g)
+    bias = torch.randn(cD, device="cuda", generator=g)
+    y = torch.zeros(rows, O, device="cuda")
+    K.gemm(x.view(rows * F, N), w, y.view(-1)[pD:], bias=bias, epilogue=L.EPI_BIAS, rows_per_group=F,
+           ld_group=O, ld_d=cD)
+    want = (x.double().view(rows, F, N) @ w.double().T + bias.double()).reshape(rows, F * cD)
+    assert torch.allclose(y[:, pD:].double(), want, rtol=1e-5, atol=1e-5)
+    assert (y[:, :pD] == 0).all()
