@@ -1,0 +1,373 @@
+"""Benchmark of the DMT / SPTT hot path on B200 (contract: see DESIGN.md §Measurement).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dmt|reference]
+
+A *step* = one SPTT training pass over one synthetic batch per GPU: step a
+bucketing + index all-to-all, pooled lookup, tower exchange, DCN tower module
+forward, synthetic upstream gradient, reverse exchange, TM backward + tower
+all-reduce + SGD, fused embedding backward/SGD.  N=1 runs BASELINE.json
+configs[1] (26 tables x 1M rows x dim 128, pooling 20, batch 8192, DCN TM);
+N>1 runs the same per-GPU workload with towers over the GPUs (weak scaling)
+and times the flat all-to-all baseline (global DCN) alongside.
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec/box (device-timed) DCN+SPTT at 1/2/4/8 B200; lookup HBM GB/s"
+UNIT = "samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="dmt", choices=["dmt", "reference"])
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--tables", type=int, default=26)
+    ap.add_argument("--rows", type=int, default=1_000_000)
+    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--pool", type=int, default=20)
+    ap.add_argument("--batch", type=int, default=8192)
+    ap.add_argument("--tm", default="dcn", choices=["dcn", "dlrm", "passthrough"])
+    ap.add_argument("--tm-out", type=int, default=64)
+    ap.add_argument("--cross-layers", type=int, default=3)
+    ap.add_argument("--towers", type=int, default=0, help="0 = auto (1 at N=1, else 2)")
+    ap.add_argument("--no-flat", action="store_true", help="skip the flat-baseline comparison at N>1")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling runs)")
+    ap.add_argument("--cpu-sample", type=int, default=256, help="samples per CPU-baseline step")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- #
+# clocks sampler (nvidia-smi during the timed region)
+# --------------------------------------------------------------------------- #
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sms.sort()
+        med = sms[len(sms) // 2] if sms else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# --------------------------------------------------------------------------- #
+# reference arm / CPU baseline: the oracle port on the host cores
+# --------------------------------------------------------------------------- #
+def cpu_reference_step_fn(args, sample: int):
+    """One bounded CPU step of the same workload: oracle pooled lookup over 26
+    tables (100k-row slices), DCN tower module forward + backward (float64
+    numpy/BLAS) and the embedding SGD update -- the reference algorithm
+    restated in oracle/ (the reference itself is forward-only Python)."""
+    import numpy as np
+
+    import oracle
+
+    rng = np.random.default_rng(0)
+    F, N, L = args.tables, args.dim, args.pool
+    rows = min(args.rows, 100_000)
+    tables = {t: rng.uniform(-1, 1, (rows, N)).astype(np.float32) for t in range(F)}
+    cfg = {"kind": args.tm if args.tm != "passthrough" else "dlrm", "out_dim": args.tm_out,
+           "per_feature_outputs": 1, "flat_outputs": 0, "cross_layers": args.cross_layers, "seed": 0}
+    w = oracle.init_tm_weights(cfg, F, N, salt=0)
+    lens = np.full(sample, L, dtype=np.int64)
+
+    def step():
+        idx = {t: rng.integers(0, rows, size=sample * L) for t in range(F)}
+        x = np.stack([oracle.pool(tables[t], lens, idx[t], "sum") for t in range(F)], axis=1)
+        y = oracle.tm_forward(x, cfg, w)
+        dx, dw = oracle.tm_backward(x, cfg, w, np.ones_like(y) / y.size)
+        for t in range(F):
+            uniq, g = oracle.embedding_row_grads(rows, lens, idx[t], dx[:, t, :])
+            tables[t][uniq] -= (0.01 * g).astype(np.float32)
+        return y
+
+    return step
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = os.cpu_count() or 1
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(v, str(n))
+    step = cpu_reference_step_fn(args, args.cpu_sample)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    val = args.cpu_sample * args.steps / dt
+    sample = (f"{args.cpu_sample} samples/step of the C2 workload ({args.tables} tables, 100k-row slices, "
+              f"dim {args.dim}, pooling {args.pool}, {args.tm} TM fwd+bwd + SGD), oracle numpy port, float64")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config(args, args.gpus),
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": n, "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def cpu_baseline(args) -> dict:
+    """Bounded (~10-30 s) run of the oracle port on this host, single process."""
+    import numpy as np  # noqa: F401
+
+    n = os.cpu_count() or 1
+    step = cpu_reference_step_fn(args, args.cpu_sample)
+    step()
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < 10.0 and k < 50:
+        step()
+        k += 1
+    dt = time.perf_counter() - t0
+    return {"value": args.cpu_sample * k / dt, "unit": UNIT, "cores": n, "kind": "port",
+            "sample": f"{k} steps x {args.cpu_sample} samples of the C2 workload (100k-row table slices), "
+                      f"oracle numpy port (float64; BLAS threads={n} for the TM GEMMs, lookup loops 1 thread)"}
+
+
+def _config(args, N):
+    T = _towers(args, N)
+    return {"workload": "C2 (BASELINE configs[1]): 26 tables x 1M rows x dim 128, pooling 20, batch 8192/GPU, "
+                        f"{args.tm} TM" if N == 1 else
+                        f"C2 per GPU, SPTT {T} towers x {N // T} GPUs, flat all-to-all alongside",
+            "tables": args.tables, "rows": args.rows, "dim": args.dim, "pooling_factor": args.pool,
+            "batch_per_gpu": args.batch, "global_batch": args.batch * N, "tm": args.tm, "tm_out_dim": args.tm_out,
+            "cross_layers": args.cross_layers, "towers": T, "gpus_per_tower": N // T, "optimizer": "sgd",
+            "parallelism": f"embedding model-parallel in tower, TM data-parallel in tower (T={T}, W={N // T})",
+            "l2": "inputs larger than L2 (tables >= 6.6 GB bf16, uniform random rows), no flush"}
+
+
+def _towers(args, N):
+    if args.towers:
+        return args.towers
+    return 1 if N == 1 else 2
+
+
+# --------------------------------------------------------------------------- #
+# the B200 arm
+# --------------------------------------------------------------------------- #
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_00877_b200 as P
+    from paper_2403_00877_b200 import _lib
+    from paper_2403_00877_b200.fabric import LoopbackFabric, NcclFabric
+    from paper_2403_00877_b200.pipeline import KJT, PhaseTimers
+    from paper_2403_00877_b200.sptt import SPTT, device_world, random_kjt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    N = world
+    if args.gpus != N and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs torchrun with {args.gpus} processes"}))
+        sys.exit(2)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    es = 2 if dtype == torch.bfloat16 else 4
+    T = _towers(args, N)
+    W = N // T
+    topo_args = (T, W, 1)
+    B, F, Nd, Lp = args.batch, args.tables, args.dim, args.pool
+    topo, layout, placement, assignment = device_world(*topo_args, F, args.rows, Nd, dtype, [rank], seed=0, device=dev)
+    pooling = {f: "sum" for f in range(F)}
+
+    def make_fabric():
+        return NcclFabric(N, rank, W, dev) if world > 1 else LoopbackFabric(1, dev)
+
+    fabric = make_fabric()
+    tm_cfg = None if args.tm == "passthrough" else P.TMConfig(kind=args.tm, out_dim=args.tm_out, cross_layers=args.cross_layers,
+                                                             per_feature_outputs=1, flat_outputs=0, seed=0)
+    model = SPTT(topo, layout, placement, assignment, pooling, B, fabric, tm=tm_cfg, dtype=dtype, device=dev,
+                 mode="sptt", lr=1e-3)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    batches = [{rank: random_kjt(F, B, args.rows, Lp, gen, dev)} for _ in range(4)]
+    gout = {rank: (torch.randn(B, model.out_width, generator=gen, device=dev) * 1e-3).to(dtype)}
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def timed(m, K, Wm, host_inputs=None):
+        for i in range(Wm):
+            m.train_step(batches[i % len(batches)], gout)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        timers = PhaseTimers()
+        m.engine.timers = timers
+        calls0 = _lib.CALLS[0]
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for i in range(K):
+            if host_inputs is None:
+                m.train_step(batches[i % len(batches)], gout)
+            else:
+                hl, hv, nnz = host_inputs[i % len(host_inputs)]
+                kj = KJT(hl.to(dev, non_blocking=True), hv.to(dev, non_blocking=True), nnz, B)
+                outs = m.train_step({rank: kj}, gout)
+                loss = torch.dot(outs[rank].view(-1).float(), gout[rank].view(-1).float())
+                loss.cpu()
+        e.record()
+        torch.cuda.synchronize()
+        barrier()
+        m.engine.timers = None
+        ms = s.elapsed_time(e)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), timers, _lib.CALLS[0] - calls0
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    total_ms, timers, calls = timed(model, args.steps, args.warmup)
+    clk = clocks.stop()
+    ms_step = total_ms / args.steps
+    value = N * B * args.steps / (total_ms / 1000.0)
+    ph = {k: v / args.steps for k, v in timers.ms().items()}
+
+    # e2e through the public API with host (pinned) inputs
+    e2e = None
+    if not args.no_e2e:
+        hosts = []
+        for bt in batches:
+            kj = bt[rank]
+            hosts.append((kj.lengths.cpu().pin_memory(), kj.values.cpu().pin_memory(), kj.nnz_per_feature))
+        e_ms, _, _ = timed(model, args.steps, 2, host_inputs=hosts)
+        h2d = hosts[0][0].numel() * 4 + hosts[0][1].numel() * 4
+        e2e = {"value": N * B * args.steps / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 4}
+
+    # roofline of the lookup kernel: algorithmic bytes per launch
+    p = model.plan
+    bags = p.owner_bags(rank)
+    nnz = bags * Lp
+    look_bytes = nnz * Nd * es + nnz * 4 + (bags + 1) * 8 + bags * Nd * es
+    import json as _j
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = _j.load(fh)
+        hbm, tf = peaks["hbm_gbs"], peaks["bf16_tflops_sustained"]
+        peak_src = "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        hbm, tf = 6650.0, 1400.0
+        peak_src = "fallback (B200_PROFILING.md)"
+    n_look = max(1, timers.count("lookup_fwd") // args.steps)
+    look_ms = ph.get("lookup_fwd", 0.0) / n_look
+    look_gbs = look_bytes / (look_ms * 1e-3) / 1e9 if look_ms else 0.0
+    roof_lookup = {"bound": "hbm", "achieved": look_gbs, "peak": hbm, "unit": "GB/s", "frac": look_gbs / hbm,
+                   "traffic": None, "kernel": "dmt::pooled_fwd_kernel", "algorithmic_bytes": look_bytes,
+                   "launch_ms": look_ms, "peak_source": peak_src}
+    roof = roof_lookup
+    if tm_cfg is not None and args.tm == "dcn":
+        t_own = p.tower_of(rank)
+        Ft = len(p.tower_features[t_own])
+        rows = p.T * B
+        fwd = P.tm_flops(tm_cfg, Ft, Nd, rows)
+        tm_flops_step = 3.0 * fwd  # fwd + (dX, dW) backward
+        tm_ms = ph.get("tm_fwd", 0.0) + ph.get("tm_bwd", 0.0)
+        if tm_ms > look_ms:
+            ach = tm_flops_step / (tm_ms * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": tf, "unit": "TFLOP/s", "frac": ach / tf,
+                    "traffic": None, "kernel": "dmt::gemm::gemm_kernel (DCN fwd+bwd GEMMs, per step)",
+                    "algorithmic_flops": tm_flops_step, "ms": tm_ms, "peak_source": peak_src + " bf16 sustained"}
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic (uniform random rows, random-init tables and TM weights)",
+        "config": _config(args, N), "roofline": roof, "roofline_lookup": roof_lookup,
+        "lookup_hbm_gbs": look_gbs, "phases_ms_per_step": ph,
+        "exposed_comm_ms_per_step": ph.get("exchange", 0.0), "clocks": clk, "e2e": e2e,
+        "gpu_launches": calls, "gpu_launches_note": "libdmt entry-point calls in the timed region (each >= 1 kernel)",
+    }
+    # flat all-to-all baseline alongside (N > 1)
+    if N > 1 and not args.no_flat:
+        del model
+        torch.cuda.empty_cache()
+        flat = SPTT(topo, layout, placement, assignment, pooling, B, fabric, tm=tm_cfg, dtype=dtype, device=dev,
+                    mode="flat", lr=1e-3)
+        gout = {rank: (torch.randn(B, flat.out_width, generator=gen, device=dev) * 1e-3).to(dtype)}
+        f_ms, f_t, _ = timed(flat, args.steps, args.warmup)
+        fph = {k: v / args.steps for k, v in f_t.ms().items()}
+        result["flat_baseline"] = {"value": N * B * args.steps / (f_ms / 1000.0), "ms_per_step": f_ms / args.steps,
+                                   "exposed_comm_ms_per_step": fph.get("exchange", 0.0), "phases_ms_per_step": fph}
+    if rank == 0 and N == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

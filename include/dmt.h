@@ -114,12 +114,13 @@ int dmt_pooled_lookup_fwd(const dmt_lookup_segment* segs, const dmt_lookup_segme
 /* Backward with fused optimizer (absent in the reference).
  * segs[i].out is the gradient of the pooled rows, segs[i].weights is updated
  * in place (const is cast away), key_base/rows define a disjoint key range per
- * shard (segments of the same shard share it).  Duplicate rows are reduced
+ * shard (segments of the same shard share it).  The segments must tile bags
+ * [0, num_bags) in order (offsets[0] == 0), as the owner's received KJT does.  Duplicate rows are reduced
  * after a stable radix sort, so the update is deterministic.
  * optimizer: 0 = SGD (w -= lr*g), 1 = row-wise Adagrad
  * (s += mean(g^2); w -= lr*g/(sqrt(s)+eps)). */
 enum dmt_optimizer { DMT_OPT_SGD = 0, DMT_OPT_ROWWISE_ADAGRAD = 1 };
-size_t dmt_pooled_lookup_bwd_workspace_size(int64_t nnz, int64_t key_space, int32_t num_segs);
+size_t dmt_pooled_lookup_bwd_workspace_size(int64_t nnz, int64_t key_space, int64_t num_bags);
 int dmt_pooled_lookup_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host,
                           int32_t num_segs, const int64_t* offsets, const int32_t* indices,
                           int64_t nnz, int64_t key_space, int32_t dtype, int32_t optimizer,
@@ -185,6 +186,12 @@ int dmt_batched_copy2d(const dmt_copy2d* copies, int32_t n, int32_t elem_bytes, 
  * so the per-feature DLRM projection can write straight into the tower output. */
 enum dmt_epilogue { DMT_EPI_NONE = 0, DMT_EPI_BIAS = 1, DMT_EPI_CROSS = 2, DMT_EPI_ACC = 3 };
 
+/* dmt_gemm_args.flags: operand stored transposed (MN-major).  TRANS_A: `a`
+ * holds A^T as a [k, m] matrix with row stride lda (m contiguous); TRANS_B:
+ * `b` holds B^T as [k, n] with row stride ldb.  Read straight by TMA, no
+ * transpose pass (dW = G^T X, dX = G W). */
+enum dmt_gemm_flags { DMT_GEMM_TRANS_A = 1, DMT_GEMM_TRANS_B = 2 };
+
 typedef struct dmt_gemm_args {
   const void* a;   /* [m, k] row stride lda */
   const void* b;   /* [n, k] row stride ldb */
@@ -200,7 +207,7 @@ typedef struct dmt_gemm_args {
   int32_t in_dtype;  /* dmt_dtype of a, b (and x0/xl/aux for CROSS) */
   int32_t out_dtype; /* dmt_dtype of d */
   int32_t epilogue;
-  int32_t pad_;
+  int32_t flags;     /* dmt_gemm_flags */
 } dmt_gemm_args;
 
 int dmt_gemm(const dmt_gemm_args* args, dmt_stream_t stream);

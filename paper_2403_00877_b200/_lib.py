@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libdmt.so")
 DT_F32, DT_BF16, DT_F64, DT_F16 = 0, 1, 2, 3
 POOL_NONE, POOL_SUM, POOL_MEAN = 0, 1, 2
 EPI_NONE, EPI_BIAS, EPI_CROSS, EPI_ACC = 0, 1, 2, 3
+GEMM_TRANS_A, GEMM_TRANS_B = 1, 2
 OPT_SGD, OPT_ROWWISE_ADAGRAD = 0, 1
 EBIT_INDEX, EBIT_BAGLEN = 1, 2
 
@@ -58,7 +59,7 @@ class GemmArgs(C.Structure):
         ("m", i64), ("n", i64), ("k", i64),
         ("lda", i64), ("ldb", i64), ("ld_d", i64), ("ld_x", i64),
         ("rows_per_group", i64), ("ld_group", i64),
-        ("beta", f32), ("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("pad_", i32),
+        ("beta", f32), ("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("flags", i32),
     ]
 
 
@@ -69,7 +70,7 @@ _SIGS = {
     "dmt_kjt_bucketize": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]),
     "dmt_kjt_slot_offsets": (C.c_int, [vp, i32, i32, vp, vp, vp]),
     "dmt_pooled_lookup_fwd": (C.c_int, [vp, vp, i32, vp, vp, i32, vp, vp]),
-    "dmt_pooled_lookup_bwd_workspace_size": (sz, [i64, i64, i32]),
+    "dmt_pooled_lookup_bwd_workspace_size": (sz, [i64, i64, i64]),
     "dmt_pooled_lookup_bwd": (C.c_int, [vp, vp, i32, vp, vp, i64, i64, i32, i32, f32, f32, vp, sz, vp]),
     "dmt_assemble": (C.c_int, [vp, i32, i32, vp, i64, vp, i64, i32, vp]),
     "dmt_batched_copy": (C.c_int, [vp, i32, i64, vp]),
@@ -114,7 +115,11 @@ def lib():
     return load_library(True)
 
 
+CALLS = [0]  # libdmt entry-point calls (each launches >= 1 kernel); read by bench.py
+
+
 def check(status: int, what: str) -> None:
+    CALLS[0] += 1
     if status != 0:
         cls = STATUS_ERRORS.get(status, TowersimError)
         raise cls(f"{what} failed with libdmt status {status}")

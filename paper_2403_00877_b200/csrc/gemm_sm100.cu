@@ -116,21 +116,53 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 //   [0,14) start>>4  [16,30) LBO>>4 (unused for swizzled K-major)
 //   [32,46) SBO>>4 = 1024 B between 8-row core groups   [46,48) version = 1
 //   [61,64) layout = 2 (SWIZZLE_128B)
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo = 16, uint32_t sbo = 1024) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
 }
 
+// Operand tile in shared memory (SWIZZLE_128B), ROWS x one 128-byte K block:
+//   K-major : ROWS rows of 128 B (K contiguous); 8-row groups 1024 B apart
+//             (SBO); one MMA K-step advances the start address by 32 B.
+//   MN-major: ROWS/ATOM columns of ATOM = 128/es MN-elements; each column is
+//             BK K-rows of 128 B (LBO = BK*128 B between columns, SBO = 1024 B
+//             between 8-K-row groups); one MMA K-step = 32/es K-rows =
+//             4096/es bytes.  This is how dW = G^T X and dX = G W read their
+//             operands without any transpose kernel.
+template <typename TIN, bool MN>
+struct Operand {
+  static constexpr int ES = sizeof(TIN);
+  static constexpr int BK = kAtomBytes / ES;       // K elements per stage
+  static constexpr int ATOM = kAtomBytes / ES;     // MN elements per 128-byte atom
+  static constexpr uint32_t COL_BYTES = BK * kAtomBytes;
+  __device__ static __forceinline__ uint64_t desc(uint32_t base) {
+    return MN ? make_desc(base, COL_BYTES, 1024) : make_desc(base, 16, 1024);
+  }
+  __device__ static __forceinline__ uint64_t kstep(int kk) {
+    return MN ? (uint64_t)(((uint32_t)kk * (4096u / ES)) >> 4) : (uint64_t)((kk * kUmmaKBytes) >> 4);
+  }
+  template <int ROWS>
+  __device__ static __forceinline__ void load(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0, int r0) {
+    if constexpr (!MN) {
+      tma_load_2d(dst, map, bar, k0, r0);
+    } else {
+#pragma unroll
+      for (int c = 0; c < ROWS / ATOM; ++c) tma_load_2d(dst + c * COL_BYTES, map, bar, r0 + c * ATOM, k0);
+    }
+  }
+};
+
 // Instruction descriptor (kind::f16 / kind::tf32), both operands K-major:
 //   [4,6) D fmt = 1 (f32)  [7,10) A fmt  [10,13) B fmt  [17,23) N>>3  [24,29) M>>4
-__host__ __device__ constexpr uint32_t make_idesc(int ab_fmt, int m, int n) {
-  return (1u << 4) | ((uint32_t)ab_fmt << 7) | ((uint32_t)ab_fmt << 10) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(m >> 4) << 24);
+//   [15] A major (1 = MN)  [16] B major (1 = MN)
+__host__ __device__ constexpr uint32_t make_idesc(int ab_fmt, int m, int n, bool a_mn = false, bool b_mn = false) {
+  return (1u << 4) | ((uint32_t)ab_fmt << 7) | ((uint32_t)ab_fmt << 10) | ((uint32_t)(a_mn ? 1 : 0) << 15) |
+         ((uint32_t)(b_mn ? 1 : 0) << 16) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 struct Params {
@@ -146,36 +178,59 @@ struct Params {
   int in_dtype;
   int epilogue;
   int vec_store;
+  int vec_x;
 };
 
-template <typename TO>
-__device__ __forceinline__ void store_row32(TO* p, const float* v, int ncols, bool vec) {
-  if (vec && ncols == 32) {
-    if constexpr (sizeof(TO) == 4) {
+// 32 consecutive elements of one row <-> 32 fp32 registers.  The vector forms
+// need 16-byte alignment; the scalar forms are predicated (tail / unaligned).
+template <typename TX>
+__device__ __forceinline__ void load32v(const TX* __restrict__ p, float* v) {
+  if constexpr (sizeof(TX) == 4) {
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 x;
-        TO* h = reinterpret_cast<TO*>(&x);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) h[j] = from_f<TO>(v[i + j]);
-        *reinterpret_cast<uint4*>(p + i) = x;
-      }
+    for (int i = 0; i < 32; i += 4) {
+      float4 x = *reinterpret_cast<const float4*>(p + i);
+      v[i] = x.x; v[i + 1] = x.y; v[i + 2] = x.z; v[i + 3] = x.w;
     }
   } else {
-    for (int i = 0; i < ncols; ++i) p[i] = from_f<TO>(v[i]);
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      uint4 x = *reinterpret_cast<const uint4*>(p + i);
+      const TX* h = reinterpret_cast<const TX*>(&x);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[i + j] = to_f<TX>(h[j]);
+    }
   }
 }
-
+template <typename TO>
+__device__ __forceinline__ void store32v(TO* __restrict__ p, const float* v) {
+  if constexpr (sizeof(TO) == 4) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      uint4 x;
+      TO* h = reinterpret_cast<TO*>(&x);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) h[j] = from_f<TO>(v[i + j]);
+      *reinterpret_cast<uint4*>(p + i) = x;
+    }
+  }
+}
 template <typename TX>
-__device__ __forceinline__ void load_row32(const TX* p, float* v, int ncols) {
-  for (int i = 0; i < ncols; ++i) v[i] = to_f<TX>(p[i]);
+__device__ __forceinline__ void load32s(const TX* __restrict__ p, float* v, int n) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = (i < n) ? to_f<TX>(p[i]) : 0.f;
+}
+template <typename TO>
+__device__ __forceinline__ void store32s(TO* __restrict__ p, const float* v, int n) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < n) p[i] = from_f<TO>(v[i]);
 }
 
 // BN: tile N (64/128/256); NOPS: 1 (plain) or 3 (3xTF32); KIND: 0 f16-family, 1 tf32
-template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO>
+template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_lo,
@@ -199,6 +254,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   const int64_t num_tiles = tiles_m * tiles_n;
   const int num_kb = (int)ceil_div(p.k * (int64_t)sizeof(TIN), kAtomBytes);
   constexpr int K_ELEMS = kAtomBytes / sizeof(TIN);
+  using OA = Operand<TIN, AMN>;
+  using OB = Operand<TIN, BMN>;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -237,13 +294,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
           mbar_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sa, &map_a, &full[stage], kb * K_ELEMS, m0);
-          tma_load_2d(sb, &map_b, &full[stage], kb * K_ELEMS, n0);
+          OA::template load<kBlockM>(sa, &map_a, &full[stage], kb * K_ELEMS, m0);
+          OB::template load<BN>(sb, &map_b, &full[stage], kb * K_ELEMS, n0);
           if constexpr (NSETS == 2) {
             uint8_t* sa2 = sb + B_BYTES;
             uint8_t* sb2 = sa2 + A_BYTES;
-            tma_load_2d(sa2, &map_a_lo, &full[stage], kb * K_ELEMS, m0);
-            tma_load_2d(sb2, &map_b_lo, &full[stage], kb * K_ELEMS, n0);
+            OA::template load<kBlockM>(sa2, &map_a_lo, &full[stage], kb * K_ELEMS, m0);
+            OB::template load<BN>(sb2, &map_b_lo, &full[stage], kb * K_ELEMS, n0);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -266,20 +323,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           tc_fence_after();
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          const uint64_t da = make_desc(smem_u32(sa));
-          const uint64_t db = make_desc(smem_u32(sb));
+          const uint64_t da = OA::desc(smem_u32(sa));
+          const uint64_t db = OB::desc(smem_u32(sb));
 #pragma unroll
           for (int kk = 0; kk < kAtomBytes / kUmmaKBytes; ++kk) {
-            const uint64_t adv = (uint64_t)((kk * kUmmaKBytes) >> 4);
+            const uint64_t ada = OA::kstep(kk), adb = OB::kstep(kk);
             const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
-            umma<KIND>(tmem_d, da + adv, db + adv, idesc, accum);
+            umma<KIND>(tmem_d, da + ada, db + adb, idesc, accum);
             if constexpr (NSETS == 2) {
               uint8_t* sa2 = sb + B_BYTES;
               uint8_t* sb2 = sa2 + A_BYTES;
-              const uint64_t da2 = make_desc(smem_u32(sa2));
-              const uint64_t db2 = make_desc(smem_u32(sb2));
-              umma<KIND>(tmem_d, da + adv, db2 + adv, idesc, 1u);  // hi * lo
-              umma<KIND>(tmem_d, da2 + adv, db + adv, idesc, 1u);  // lo * hi
+              const uint64_t da2 = OA::desc(smem_u32(sa2));
+              const uint64_t db2 = OB::desc(smem_u32(sb2));
+              umma<KIND>(tmem_d, da + ada, db2 + adb, idesc, 1u);  // hi * lo
+              umma<KIND>(tmem_d, da2 + ada, db + adb, idesc, 1u);  // lo * hi
             }
           }
           umma_commit(&empty[stage]);  // smem slot reusable once these MMAs retire
@@ -312,23 +369,50 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         const int64_t rem = p.n - col;
         const int ncols = rem <= 0 ? 0 : (rem < 32 ? (int)rem : 32);
         if (!row_ok || ncols == 0) continue;
+        const bool full = ncols == 32;
         if (p.epilogue == DMT_EPI_BIAS || p.epilogue == DMT_EPI_CROSS) {
-          for (int i = 0; i < ncols; ++i) v[i] += p.bias[col + i];
+          if (full) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              float4 bb = __ldg(reinterpret_cast<const float4*>(p.bias + col + i));
+              v[i] += bb.x; v[i + 1] += bb.y; v[i + 2] += bb.z; v[i + 3] += bb.w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += (i < ncols) ? p.bias[col + i] : 0.f;
+          }
         }
         if (p.epilogue == DMT_EPI_CROSS) {
-          float x0v[32], xlv[32];
           const TIN* x0p = reinterpret_cast<const TIN*>(p.x0) + row * p.ld_x + col;
           const TIN* xlp = reinterpret_cast<const TIN*>(p.xl) + row * p.ld_x + col;
-          load_row32<TIN>(x0p, x0v, ncols);
-          load_row32<TIN>(xlp, xlv, ncols);
-          if (p.aux) store_row32<TIN>(reinterpret_cast<TIN*>(p.aux) + row * p.ld_x + col, v, ncols, false);
-          for (int i = 0; i < ncols; ++i) v[i] = x0v[i] * v[i] + xlv[i];
+          TIN* auxp = p.aux ? reinterpret_cast<TIN*>(p.aux) + row * p.ld_x + col : nullptr;
+          float t[32];
+          if (full && p.vec_x) {
+            if (auxp) store32v<TIN>(auxp, v);
+            load32v<TIN>(x0p, t);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= t[i];
+            load32v<TIN>(xlp, t);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += t[i];
+          } else {
+            if (auxp) store32s<TIN>(auxp, v, ncols);
+            load32s<TIN>(x0p, t, ncols);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= t[i];
+            load32s<TIN>(xlp, t, ncols);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += t[i];
+          }
         } else if (p.epilogue == DMT_EPI_ACC) {
-          float old[32];
-          load_row32<TO>(drow + col, old, ncols);
-          for (int i = 0; i < ncols; ++i) v[i] += p.beta * old[i];
+          float t[32];
+          if (full && p.vec_store) load32v<TO>(drow + col, t);
+          else load32s<TO>(drow + col, t, ncols);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += p.beta * t[i];
         }
-        store_row32<TO>(drow + col, v, ncols, p.vec_store != 0);
+        if (full && p.vec_store) store32v<TO>(drow + col, v);
+        else store32s<TO>(drow + col, v, ncols);
       }
       tc_fence_before();
       __syncwarp();
@@ -357,8 +441,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// K-major operand [rows, k] (row stride ld): box {128 B of K, box_rows}.
+// MN-major operand stored [k, rows] (row stride ld): box {128 B of MN, 128 B / es K-rows}.
 static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int64_t ld, int dtype,
-                     int box_rows) {
+                     int box_rows, bool mn = false) {
   auto fn = encode_fn();
   if (!fn) return false;
   CUtensorMapDataType t;
@@ -372,24 +458,30 @@ static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k,
   cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
   cuuint32_t box[2] = {(cuuint32_t)(kAtomBytes / es), (cuuint32_t)box_rows};
+  if (mn) {
+    dims[0] = (cuuint64_t)rows;
+    dims[1] = (cuuint64_t)k;
+    box[0] = (cuuint32_t)(kAtomBytes / es);
+    box[1] = (cuuint32_t)(kAtomBytes / es);
+  }
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, t, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO>
+template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN>
 static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cudaStream_t s) {
   constexpr int NSETS = (NOPS == 3) ? 2 : 1;
   constexpr int STAGE_BYTES = NSETS * (kBlockM + BN) * kAtomBytes;
   constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(SMEM <= 232448, "smem");
   CUtensorMap ma, mb, mal, mbl;
-  if (!make_map(&ma, a->a, a->m, a->k, a->lda, a->in_dtype, kBlockM)) return DMT_ERR_CUDA;
-  if (!make_map(&mb, a->b, a->n, a->k, a->ldb, a->in_dtype, BN)) return DMT_ERR_CUDA;
+  if (!make_map(&ma, a->a, a->m, a->k, a->lda, a->in_dtype, kBlockM, AMN)) return DMT_ERR_CUDA;
+  if (!make_map(&mb, a->b, a->n, a->k, a->ldb, a->in_dtype, BN, BMN)) return DMT_ERR_CUDA;
   if (NSETS == 2) {
-    if (!make_map(&mal, a_lo, a->m, a->k, a->lda, a->in_dtype, kBlockM)) return DMT_ERR_CUDA;
-    if (!make_map(&mbl, b_lo, a->n, a->k, a->ldb, a->in_dtype, BN)) return DMT_ERR_CUDA;
+    if (!make_map(&mal, a_lo, a->m, a->k, a->lda, a->in_dtype, kBlockM, AMN)) return DMT_ERR_CUDA;
+    if (!make_map(&mbl, b_lo, a->n, a->k, a->ldb, a->in_dtype, BN, BMN)) return DMT_ERR_CUDA;
   } else {
     mal = ma;
     mbl = mb;
@@ -403,7 +495,11 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   p.beta = a->beta; p.out_dtype = a->out_dtype; p.in_dtype = a->in_dtype; p.epilogue = a->epilogue;
   size_t eo = dtype_size(a->out_dtype);
   p.vec_store = ((uintptr_t)a->d % 16 == 0) && ((a->ld_d * eo) % 16 == 0) && ((a->ld_group * eo) % 16 == 0);
-  auto kern = gemm_kernel<BN, NOPS, KIND, STAGES, TIN, TO>;
+  size_t ei = dtype_size(a->in_dtype);
+  p.vec_x = ((uintptr_t)a->x0 % 16 == 0) && ((uintptr_t)a->xl % 16 == 0) && ((uintptr_t)a->aux % 16 == 0) &&
+            ((a->ld_x * ei) % 16 == 0);
+  if (a->bias && ((uintptr_t)a->bias % 16)) return DMT_ERR_UNSUPPORTED;
+  auto kern = gemm_kernel<BN, NOPS, KIND, STAGES, TIN, TO, AMN, BMN>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
@@ -413,30 +509,39 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   int64_t tiles = ceil_div(a->m, kBlockM) * ceil_div(a->n, BN);
   int grid = (int)std::min<int64_t>(tiles, DMT_NUM_SMS);
   const int fmt = (KIND == 1) ? 2 : (std::is_same<TIN, __half>::value ? 0 : 1);
-  uint32_t idesc = make_idesc(fmt, kBlockM, BN);
+  uint32_t idesc = make_idesc(fmt, kBlockM, BN, AMN, BMN);
   kern<<<grid, kThreads, SMEM, s>>>(ma, mb, mal, mbl, p, idesc);
   DMT_CHECK_LAUNCH();
   return DMT_OK;
 }
 
-template <typename TIN, typename TO>
+template <typename TIN, typename TO, bool AMN, bool BMN>
 static int dispatch_n(const dmt_gemm_args* a, const void* alo, const void* blo, cudaStream_t s) {
   if constexpr (std::is_same<TIN, float>::value) {
-    if (a->n <= 64) return launch<64, 3, 1, 4, TIN, TO>(a, alo, blo, s);
-    return launch<128, 3, 1, 3, TIN, TO>(a, alo, blo, s);
+    if (a->n <= 64) return launch<64, 3, 1, 4, TIN, TO, AMN, BMN>(a, alo, blo, s);
+    return launch<128, 3, 1, 3, TIN, TO, AMN, BMN>(a, alo, blo, s);
   } else {
-    if (a->n <= 64) return launch<64, 1, 0, 8, TIN, TO>(a, alo, blo, s);
-    if (a->n <= 128) return launch<128, 1, 0, 6, TIN, TO>(a, alo, blo, s);
-    return launch<256, 1, 0, 4, TIN, TO>(a, alo, blo, s);
+    if (a->n <= 64) return launch<64, 1, 0, 8, TIN, TO, AMN, BMN>(a, alo, blo, s);
+    if (a->n <= 128) return launch<128, 1, 0, 6, TIN, TO, AMN, BMN>(a, alo, blo, s);
+    return launch<256, 1, 0, 4, TIN, TO, AMN, BMN>(a, alo, blo, s);
   }
+}
+
+template <typename TIN, typename TO>
+static int dispatch_major(const dmt_gemm_args* a, const void* alo, const void* blo, cudaStream_t s) {
+  const bool amn = (a->flags & DMT_GEMM_TRANS_A) != 0, bmn = (a->flags & DMT_GEMM_TRANS_B) != 0;
+  if (!amn && !bmn) return dispatch_n<TIN, TO, false, false>(a, alo, blo, s);
+  if (amn && bmn) return dispatch_n<TIN, TO, true, true>(a, alo, blo, s);
+  if (bmn) return dispatch_n<TIN, TO, false, true>(a, alo, blo, s);
+  return dispatch_n<TIN, TO, true, false>(a, alo, blo, s);
 }
 
 template <typename TIN>
 static int dispatch_out(const dmt_gemm_args* a, const void* alo, const void* blo, cudaStream_t s) {
   switch (a->out_dtype) {
-    case DMT_F32: return dispatch_n<TIN, float>(a, alo, blo, s);
-    case DMT_BF16: return dispatch_n<TIN, __nv_bfloat16>(a, alo, blo, s);
-    case DMT_F16: return dispatch_n<TIN, __half>(a, alo, blo, s);
+    case DMT_F32: return dispatch_major<TIN, float>(a, alo, blo, s);
+    case DMT_BF16: return dispatch_major<TIN, __nv_bfloat16>(a, alo, blo, s);
+    case DMT_F16: return dispatch_major<TIN, __half>(a, alo, blo, s);
     default: return DMT_ERR_UNSUPPORTED;
   }
 }

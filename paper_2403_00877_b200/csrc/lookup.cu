@@ -244,130 +244,156 @@ int launch_fwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
 }
 
 // ----------------------------------------------------------------------------
-// Backward: key build -> stable radix sort -> run-length encode -> per-row
-// reduction in sorted (= original occurrence) order -> fused optimizer.
+// Backward: (1) per-occurrence sort keys (shard key base + local row) and per-
+// bag metadata (gradient row pointer, 1/len for mean, segment id); (2) stable
+// radix sort of (key, bag) pairs; (3) one pass over the sorted occurrences:
+// the thread group whose chunk holds a run's first occurrence reduces the run
+// in sorted (= original occurrence) order and applies SGD / row-wise Adagrad to
+// that row once -- deterministic, no atomics.  Each group owns kChunk
+// consecutive occurrences and issues the loads of all its run heads together
+// (memory-level parallelism; runs are 1-2 long for uniform indices).
 // ----------------------------------------------------------------------------
-constexpr uint32_t kInvalidKeyOffset = 0;  // invalid key = key_space
+constexpr int kChunk = 4;
 
-__device__ __forceinline__ int find_seg(const dmt_lookup_segment* __restrict__ segs, int n, int64_t gb) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {  // last seg with bag_begin <= gb
-    int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].bag_begin <= gb) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
+// Everything the update needs about a bag, in one 32-byte record (two 16-byte
+// loads from the same sector): gradient row, "virtual" weight / state bases
+// (already offset by -key_base, so row = base + key * ld), 1/len for mean.
+struct __align__(16) BagRec {
+  const void* grad;
+  const char* wvbase;
+  float* svbase;
+  float scale;
+  uint16_t ld;
+  uint16_t width;
+};
 
-// One thread per bag of one segment: emits (key, bag) for each occurrence.
+// group of 8 threads per bag: coalesced key/value writes
 __global__ void bwd_keys_kernel(const dmt_lookup_segment* __restrict__ segs, const int64_t* __restrict__ offsets,
-                                const int32_t* __restrict__ indices, int64_t base_off, uint32_t invalid,
-                                uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+                                const int32_t* __restrict__ indices, uint32_t invalid, uint32_t* __restrict__ keys,
+                                int32_t* __restrict__ vals, BagRec* __restrict__ recs, int es) {
   const dmt_lookup_segment& sg = segs[blockIdx.y];
-  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int sub = threadIdx.x & 7;
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   if (b >= sg.nbags) return;
-  int64_t gb = sg.bag_begin + b;
-  int64_t beg = offsets[gb], end = offsets[gb + 1];
-  for (int64_t k = beg; k < end; ++k) {
-    int64_t r = (int64_t)indices[k] - sg.row_begin;
+  const int64_t gb = sg.bag_begin + b;
+  const int64_t beg = offsets[gb], end = offsets[gb + 1];
+  for (int64_t k = beg + sub; k < end; k += 8) {
+    int64_t r = (int64_t)__ldg(indices + k) - sg.row_begin;
     bool in = r >= 0 && r < sg.rows;
-    keys[k - base_off] = in ? (uint32_t)(sg.key_base + r) : invalid;
-    vals[k - base_off] = (int32_t)gb;
+    keys[k] = in ? (uint32_t)(sg.key_base + r) : invalid;
+    vals[k] = (int32_t)gb;
+  }
+  if (sub == 0) {
+    BagRec rec;
+    rec.grad = reinterpret_cast<const char*>(sg.out) + (size_t)(b * sg.out_ld) * es;
+    rec.wvbase = reinterpret_cast<const char*>(sg.weights) - (ptrdiff_t)(sg.key_base * sg.ld) * es;
+    rec.svbase = sg.state ? reinterpret_cast<float*>(sg.state) - sg.key_base : nullptr;
+    rec.scale = (sg.pooling == DMT_POOL_MEAN && end > beg) ? 1.f / (float)(end - beg) : 1.f;
+    rec.ld = (uint16_t)sg.ld;
+    rec.width = (uint16_t)sg.width;
+    recs[gb] = rec;
   }
 }
 
-template <typename T, int VEC>
-__global__ void __launch_bounds__(kLookupThreads)
-bwd_update_kernel(const dmt_lookup_segment* __restrict__ segs, int nsegs, const int64_t* __restrict__ offsets,
-                  const uint32_t* __restrict__ ukeys, const int64_t* __restrict__ run_off,
-                  const int32_t* __restrict__ num_runs_p, const int32_t* __restrict__ sorted_bags,
-                  uint32_t invalid, int log2g, int nv, int opt, float lr, float eps) {
+template <typename T, int VEC, int NV, int CH>
+__global__ void __launch_bounds__(kLookupThreads, 2)
+bwd_update_kernel(const uint32_t* __restrict__ skeys, const int32_t* __restrict__ sbags, int64_t nnz,
+                  const BagRec* __restrict__ recs, uint32_t invalid, int log2g, int opt, float lr, float eps) {
   using A = typename Acc<T>::type;
   const int G = 1 << log2g;
-  const int gid = threadIdx.x >> log2g, t = threadIdx.x & (G - 1);
-  const int groups_per_block = kLookupThreads >> log2g;
-  const int num_runs = *num_runs_p;
-  // warp-uniform trip count: every lane of a warp runs the same iterations so
-  // the Adagrad shuffles below never diverge.
-  for (int64_t base = (int64_t)blockIdx.x * groups_per_block; base < num_runs;
-       base += (int64_t)gridDim.x * groups_per_block) {
-    const int64_t run = base + gid;
-    bool valid = run < num_runs;
-    uint32_t key = valid ? ukeys[run] : invalid;
-    valid = valid && key != invalid;
-    int64_t r0 = 0, r1 = 0, row = 0;
-    const dmt_lookup_segment* s0 = segs;
-    if (valid) {
-      r0 = run_off[run];
-      r1 = run_off[run + 1];
-      s0 = &segs[find_seg(segs, nsegs, sorted_bags[r0])];
-      row = (int64_t)key - s0->key_base;
-    }
-    T* __restrict__ W = const_cast<T*>(reinterpret_cast<const T*>(s0->weights)) + row * s0->ld;
-    const int width = valid ? s0->width : 0;
-    for (int vbase = 0; vbase < nv; vbase += 4) {
-      A acc[4][VEC];
+  const int t = threadIdx.x & (G - 1);
+  const int gpw = 32 >> log2g;                      // groups per warp
+  const int gin = (threadIdx.x & 31) >> log2g;      // group index inside the warp
+  const int64_t warp_global = (int64_t)blockIdx.x * (kLookupThreads / 32) + (threadIdx.x >> 5);
+  const int64_t stride = (int64_t)gridDim.x * (kLookupThreads / 32) * gpw * CH;
+  // warp-uniform trip count: the Adagrad shuffles below never diverge
+  for (int64_t base = warp_global * gpw * CH; base < nnz; base += stride) {
+    const int64_t c0 = base + (int64_t)gin * CH;
+    uint32_t k[CH + 1];
+    const uint32_t prev = (c0 > 0 && c0 <= nnz) ? __ldg(skeys + c0 - 1) : 0xFFFFFFFFu;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+    for (int u = 0; u <= CH; ++u) k[u] = (c0 + u < nnz) ? __ldg(skeys + c0 + u) : 0xFFFFFFFEu;
+    bool head[CH];
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) acc[q][e] = A(0);
-      for (int64_t i = r0; i < r1; ++i) {
-        int64_t gb = sorted_bags[i];
-        const dmt_lookup_segment& sg = segs[find_seg(segs, nsegs, gb)];
-        const T* gp = reinterpret_cast<const T*>(sg.out) + (gb - sg.bag_begin) * sg.out_ld;
-        A scale = A(1);
-        if (sg.pooling == DMT_POOL_MEAN) scale = A(1) / (A)(offsets[gb + 1] - offsets[gb]);
+    for (int u = 0; u < CH; ++u) head[u] = (c0 + u < nnz) && k[u] != invalid && k[u] != (u ? k[u - 1] : prev);
+    // level 1: bag records of the run heads
+    BagRec rec[CH];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          int c = ((vbase + q) * G + t) * VEC;
-          if (vbase + q < nv && c < width) {
-            A v[VEC];
-            Loader<T, VEC>::load(gp + c, v);
+    for (int u = 0; u < CH; ++u)
+      if (head[u]) rec[u] = recs[__ldg(sbags + c0 + u)];
+    // level 2: first gradient row and the weight row of every head, issued
+    // together and kept raw until the update
+    Frag<T, VEC> g0[CH][NV], w[CH][NV];
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) acc[q][e] += scale * v[e];
+    for (int u = 0; u < CH; ++u)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int c = (v * G + t) * VEC;
+        if (head[u] && c < rec[u].width) {
+          g0[u][v].load(reinterpret_cast<const T*>(rec[u].grad) + c);
+          w[u][v].load(reinterpret_cast<const T*>(rec[u].wvbase) + (int64_t)k[u] * rec[u].ld + c);
+        } else {
+          g0[u][v].zero();
+          w[u][v].zero();
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      A acc[NV][VEC];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[v][e] = A(0);
+        g0[u][v].add_to(acc[v]);
+        const A sc = head[u] ? (A)rec[u].scale : A(0);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[v][e] *= sc;
+      }
+      // further occurrences of this row (rare for uniform indices), sorted order
+      if (head[u] && k[u + 1] == k[u]) {
+        for (int64_t j = c0 + u + 1; j < nnz && __ldg(skeys + j) == k[u]; ++j) {
+          const BagRec r2 = recs[__ldg(sbags + j)];
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const int c = (v * G + t) * VEC;
+            if (c < rec[u].width) {
+              A x[VEC];
+              Loader<T, VEC>::load(reinterpret_cast<const T*>(r2.grad) + c, x);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) acc[v][e] += (A)r2.scale * x[e];
+            }
           }
         }
       }
-      if (opt == DMT_OPT_SGD) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          int c = ((vbase + q) * G + t) * VEC;
-          if (vbase + q < nv && c < width) {
-            A w[VEC];
-            Loader<T, VEC>::load(W + c, w);
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) w[e] = w[e] - (A)lr * acc[q][e];
-            Loader<T, VEC>::store(W + c, w);
-          }
-        }
-      } else {
-        // row-wise Adagrad needs mean(g^2) over the whole row: single pass
-        // (host guarantees nv <= 4 for Adagrad).
+      A step = (A)lr;
+      if (opt == DMT_OPT_ROWWISE_ADAGRAD) {
         float sq = 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          int c = ((vbase + q) * G + t) * VEC;
-          if (vbase + q < nv && c < width)
+        for (int v = 0; v < NV; ++v)
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) sq += (float)(acc[q][e] * acc[q][e]);
-        }
+          for (int e = 0; e < VEC; ++e) sq += (float)(acc[v][e] * acc[v][e]);
         for (int o = G >> 1; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o, G);
-        if (valid) {
-          float* st = reinterpret_cast<float*>(s0->state) + row;
-          float s_new = *st + sq / (float)width;
-          float denom = sqrtf(s_new) + eps;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            int c = ((vbase + q) * G + t) * VEC;
-            if (vbase + q < nv && c < width) {
-              A w[VEC];
-              Loader<T, VEC>::load(W + c, w);
-#pragma unroll
-              for (int e = 0; e < VEC; ++e) w[e] = w[e] - (A)(lr / denom) * acc[q][e];
-              Loader<T, VEC>::store(W + c, w);
-            }
-          }
-          __syncwarp((G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (threadIdx.x & 31 & ~(G - 1))));
+        if (head[u]) {
+          float* st = rec[u].svbase + k[u];
+          const float s_new = *st + sq / (float)rec[u].width;
+          step = (A)(lr / (sqrtf(s_new) + eps));
+          __syncwarp(__activemask());
           if (t == 0) *st = s_new;
+        }
+      }
+      if (!head[u]) continue;
+      T* W = const_cast<T*>(reinterpret_cast<const T*>(rec[u].wvbase)) + (int64_t)k[u] * rec[u].ld;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int c = (v * G + t) * VEC;
+        if (c < rec[u].width) {
+          A nw[VEC];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) nw[e] = A(0);
+          w[u][v].add_to(nw);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) nw[e] = nw[e] - step * acc[v][e];
+          Loader<T, VEC>::store(W + c, nw);
         }
       }
     }
@@ -375,7 +401,7 @@ bwd_update_kernel(const dmt_lookup_segment* __restrict__ segs, int nsegs, const 
 }
 
 struct BwdLayout {
-  size_t keys_in, keys_out, vals_in, vals_out, ukeys, counts, nruns, run_off, scan, cub_temp, total;
+  size_t keys_in, keys_out, vals_in, vals_out, recs, cub_temp, total;
   size_t cub_bytes;
 };
 
@@ -383,30 +409,25 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 inline int end_bit_for(uint64_t key_space) {
   int bits = 1;
-  while (bits < 32 && (1ull << bits) <= key_space) ++bits;  // need to represent key_space (invalid)
+  while (bits < 32 && (1ull << bits) <= key_space) ++bits;  // must represent key_space (= invalid)
   return bits;
 }
 
-inline BwdLayout bwd_layout(int64_t nnz, int64_t key_space) {
+inline BwdLayout bwd_layout(int64_t nnz, int64_t key_space, int64_t nbags) {
   BwdLayout L{};
   size_t n = (size_t)(nnz > 0 ? nnz : 1);
-  size_t sort_bytes = 0, rle_bytes = 0;
+  size_t nb = (size_t)(nbags > 0 ? nbags : 1);
+  size_t sort_bytes = 0;
   cub::DeviceRadixSort::SortPairs((void*)nullptr, sort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                   (const int32_t*)nullptr, (int32_t*)nullptr, (int)n, 0,
                                   end_bit_for((uint64_t)key_space));
-  cub::DeviceRunLengthEncode::Encode((void*)nullptr, rle_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                     (int32_t*)nullptr, (int32_t*)nullptr, (int)n);
-  L.cub_bytes = sort_bytes > rle_bytes ? sort_bytes : rle_bytes;
+  L.cub_bytes = sort_bytes;
   size_t off = 0;
   L.keys_in = off; off = align256(off + n * 4);
   L.keys_out = off; off = align256(off + n * 4);
   L.vals_in = off; off = align256(off + n * 4);
   L.vals_out = off; off = align256(off + n * 4);
-  L.ukeys = off; off = align256(off + n * 4);
-  L.counts = off; off = align256(off + n * 4);
-  L.nruns = off; off = align256(off + 16);
-  L.run_off = off; off = align256(off + (n + 1) * 8);
-  L.scan = off; off = align256(off + dmt_lengths_to_offsets_workspace_size((int64_t)n));
+  L.recs = off; off = align256(off + nb * sizeof(BagRec));
   L.cub_temp = off; off = align256(off + L.cub_bytes);
   L.total = off;
   return L;
@@ -416,48 +437,37 @@ template <typename T>
 int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int32_t n, const int64_t* offsets,
                const int32_t* indices, int64_t nnz, int64_t key_space, int32_t opt, float lr, float eps,
                void* ws, size_t ws_bytes, cudaStream_t s) {
-  if (nnz <= 0) return DMT_OK;
+  if (nnz <= 0 || n == 0) return DMT_OK;
   if ((uint64_t)key_space >= 0xFFFFFFFFull || nnz > 0x7FFFFFFF) return DMT_ERR_UNSUPPORTED;
-  BwdLayout L = bwd_layout(nnz, key_space);
+  int max_b = 0, max_w = 0;
+  int64_t nbags = 0;
+  for (int i = 0; i < n; ++i) {
+    if (hs[i].nbags > max_b) max_b = hs[i].nbags;
+    if (hs[i].width > max_w) max_w = hs[i].width;
+    // the segments must tile bags [0, nbags) contiguously (offsets[0] == 0)
+    if (hs[i].bag_begin != nbags) return DMT_ERR_PROTOCOL;
+    nbags += hs[i].nbags;
+    if (opt == DMT_OPT_ROWWISE_ADAGRAD && !hs[i].state) return DMT_ERR_DOMAIN;
+    if (hs[i].ld > 65535 || hs[i].width > 65535) return DMT_ERR_UNSUPPORTED;
+  }
+  if (max_b == 0) return DMT_OK;
+  BwdLayout L = bwd_layout(nnz, key_space, nbags);
   if (ws_bytes < L.total) return DMT_ERR_DOMAIN;
   char* w = (char*)ws;
   uint32_t* keys_in = (uint32_t*)(w + L.keys_in);
   uint32_t* keys_out = (uint32_t*)(w + L.keys_out);
   int32_t* vals_in = (int32_t*)(w + L.vals_in);
   int32_t* vals_out = (int32_t*)(w + L.vals_out);
-  uint32_t* ukeys = (uint32_t*)(w + L.ukeys);
-  int32_t* counts = (int32_t*)(w + L.counts);
-  int32_t* nruns = (int32_t*)(w + L.nruns);
-  int64_t* run_off = (int64_t*)(w + L.run_off);
-  void* scan_ws = (void*)(w + L.scan);
-  void* cub_ws = (void*)(w + L.cub_temp);
+  BagRec* recs = (BagRec*)(w + L.recs);
   const uint32_t invalid = (uint32_t)key_space;
 
-  // the segments must tile bags [first.bag_begin, ...) contiguously
-  int max_b = 0, max_w = 0;
-  for (int i = 0; i < n; ++i) {
-    if (hs[i].nbags > max_b) max_b = hs[i].nbags;
-    if (hs[i].width > max_w) max_w = hs[i].width;
-    if (i > 0 && hs[i].bag_begin != hs[i - 1].bag_begin + hs[i - 1].nbags) return DMT_ERR_PROTOCOL;
-  }
-  if (max_b == 0 || n == 0) return DMT_OK;
-  // base offset: offsets[first bag] -- read on device would need a sync; the
-  // caller passes indices already based at the first bag's offset (= 0 in the
-  // pipeline: segments cover the owner's whole received KJT).
-  dim3 kg((unsigned)ceil_div(max_b, 256), n);
-  bwd_keys_kernel<<<kg, 256, 0, s>>>(segs, offsets, indices, 0, invalid, keys_in, vals_in);
+  dim3 kg((unsigned)ceil_div((int64_t)max_b * 8, 256), n);
+  bwd_keys_kernel<<<kg, 256, 0, s>>>(segs, offsets, indices, invalid, keys_in, vals_in, recs, (int)sizeof(T));
   DMT_CHECK_LAUNCH();
   size_t cub_bytes = L.cub_bytes;
-  if (cub::DeviceRadixSort::SortPairs(cub_ws, cub_bytes, keys_in, keys_out, vals_in, vals_out, (int)nnz, 0,
-                                      end_bit_for((uint64_t)key_space), s) != cudaSuccess)
+  if (cub::DeviceRadixSort::SortPairs((void*)(w + L.cub_temp), cub_bytes, keys_in, keys_out, vals_in, vals_out,
+                                      (int)nnz, 0, end_bit_for((uint64_t)key_space), s) != cudaSuccess)
     return DMT_ERR_CUDA;
-  cub_bytes = L.cub_bytes;
-  if (cub::DeviceRunLengthEncode::Encode(cub_ws, cub_bytes, keys_out, ukeys, counts, nruns, (int)nnz, s) !=
-      cudaSuccess)
-    return DMT_ERR_CUDA;
-  // run offsets: exclusive scan of counts (n runs <= nnz; tail counts unused)
-  int rc = dmt_lengths_to_offsets(counts, nnz, run_off, scan_ws, (dmt_stream_t)s);
-  if (rc != DMT_OK) return rc;
   constexpr int VEC = Vec16<T>::N;
   bool vec_ok = true;
   for (int i = 0; i < n; ++i) {
@@ -465,22 +475,40 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     if (g.width % VEC || g.ld % VEC || g.out_ld % VEC || ((uintptr_t)g.weights & 15) || ((uintptr_t)g.out & 15))
       vec_ok = false;
   }
-  int grid = DMT_NUM_SMS * 8;
+  auto grid_for = [&](int log2g) {
+    const int gpb = kLookupThreads >> log2g;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ceil_div(nnz, 4), gpb), (int64_t)DMT_NUM_SMS * 12));
+  };
   if (vec_ok) {
-    int nvec = (max_w + VEC - 1) / VEC;
+    const int nvec = (max_w + VEC - 1) / VEC;
     int G = 1, log2g = 0;
     while (G < nvec && G < 32) { G <<= 1; ++log2g; }
-    int nv = (nvec + G - 1) / G;
-    if (opt == DMT_OPT_ROWWISE_ADAGRAD && nv > 4) return DMT_ERR_UNSUPPORTED;
-    bwd_update_kernel<T, VEC><<<grid, kLookupThreads, 0, s>>>(segs, n, offsets, ukeys, run_off, nruns, vals_out,
-                                                              invalid, log2g, nv, opt, lr, eps);
+    const int nv = (nvec + G - 1) / G;
+    if (nv == 1)
+      bwd_update_kernel<T, VEC, 1, 4><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+    else if (nv == 2)
+      bwd_update_kernel<T, VEC, 2, 2><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+    else if (nv <= 4)
+      bwd_update_kernel<T, VEC, 4, 1><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+    else
+      return DMT_ERR_UNSUPPORTED;
   } else {
+    if (max_w > 32 * 8) return DMT_ERR_UNSUPPORTED;
     int G = 1, log2g = 0;
     while (G < max_w && G < 32) { G <<= 1; ++log2g; }
-    int nv = (max_w + G - 1) / G;
-    if (opt == DMT_OPT_ROWWISE_ADAGRAD && nv > 4) return DMT_ERR_UNSUPPORTED;
-    bwd_update_kernel<T, 1><<<grid, kLookupThreads, 0, s>>>(segs, n, offsets, ukeys, run_off, nruns, vals_out,
-                                                            invalid, log2g, nv, opt, lr, eps);
+    const int nv = (max_w + G - 1) / G;
+    if (nv == 1)
+      bwd_update_kernel<T, 1, 1, 4><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+    else if (nv <= 4)
+      bwd_update_kernel<T, 1, 4, 1><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+    else
+      bwd_update_kernel<T, 1, 8, 1><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
   }
   DMT_CHECK_LAUNCH();
   return DMT_OK;
@@ -505,9 +533,8 @@ int dmt_pooled_lookup_fwd(const dmt_lookup_segment* segs, const dmt_lookup_segme
   }
 }
 
-size_t dmt_pooled_lookup_bwd_workspace_size(int64_t nnz, int64_t key_space, int32_t num_segs) {
-  (void)num_segs;
-  return dmt::bwd_layout(nnz, key_space).total;
+size_t dmt_pooled_lookup_bwd_workspace_size(int64_t nnz, int64_t key_space, int64_t num_bags) {
+  return dmt::bwd_layout(nnz, key_space, num_bags).total;
 }
 
 int dmt_pooled_lookup_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host, int32_t num_segs,

@@ -129,8 +129,8 @@ def raise_lookup_errors(err: torch.Tensor) -> None:
         raise TableLookupError("embedding index out of range")
 
 
-def pooled_lookup_bwd_workspace(nnz: int, key_space: int, nsegs: int, device) -> torch.Tensor:
-    n = L.lib().dmt_pooled_lookup_bwd_workspace_size(nnz, key_space, nsegs)
+def pooled_lookup_bwd_workspace(nnz: int, key_space: int, nbags: int, device) -> torch.Tensor:
+    n = L.lib().dmt_pooled_lookup_bwd_workspace_size(nnz, key_space, nbags)
     return torch.empty(max(1, n), dtype=torch.uint8, device=device)
 
 
@@ -260,22 +260,33 @@ def split_tf32(x: torch.Tensor):
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[torch.Tensor] = None,
          epilogue: int = L.EPI_NONE, x0=None, xl=None, aux=None, beta: float = 0.0,
          rows_per_group: int = 0, ld_group: int = 0, ld_d: Optional[int] = None,
-         b_split=None) -> torch.Tensor:
-    """out[m, n] = epi(a[m, k] @ b[n, k]^T).  a, b: bf16/f16/f32 (f32 -> 3xTF32).
-
-    ``b_split`` may carry a cached (hi, lo) split of an fp32 weight."""
-    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[1]:
-        raise ShapeError(f"gemm shapes {tuple(a.shape)} x {tuple(b.shape)}^T")
+         b_split=None, trans_a: bool = False, trans_b: bool = False) -> torch.Tensor:
+    """out[m, n] = epi(sum_k A[m, k] B[n, k]) on tcgen05 (bf16/f16 -> kind::f16,
+    fp32 -> 3xTF32).  A = a (m, k), or a^T when ``trans_a`` (a stored (k, m));
+    B = b (n, k), or b^T when ``trans_b`` (b stored (k, n)).  Transposed
+    operands are read MN-major by TMA (no transpose pass).  ``b_split`` may
+    carry a cached (hi, lo) tf32 split of an fp32 b."""
+    if a.dim() != 2 or b.dim() != 2:
+        raise ShapeError("gemm operands must be 2-D")
+    m, k = (a.shape[1], a.shape[0]) if trans_a else (a.shape[0], a.shape[1])
+    n, kb = (b.shape[1], b.shape[0]) if trans_b else (b.shape[0], b.shape[1])
+    if k != kb:
+        raise ShapeError(f"gemm inner dims differ: {k} vs {kb}")
     if a.dtype != b.dtype:
         raise DomainError("gemm operands must share a dtype")
-    m, k = a.shape
-    n = b.shape[0]
     if m == 0 or n == 0:
         return out
-    in_dt = _dt(a)
     if k == 0:
         raise ShapeError("gemm with k == 0")
+    in_dt = _dt(a)
     a_lo = b_lo = None
+    if a.dtype == torch.float32 and (trans_a or trans_b):
+        # tcgen05 kind::tf32 takes K-major operands only (MN-major is a 16-bit
+        # feature, like wgmma's transpose); the fp32 parity path transposes.
+        if trans_a:
+            a, trans_a = transpose(a), False
+        if trans_b:
+            b, trans_b, b_split = transpose(b), False, None
     if a.dtype == torch.float32:
         a_hi, a_lo = split_tf32(_aligned_operand(a))
         if b_split is not None:
@@ -288,12 +299,13 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[
         b = _aligned_operand(b)
     if bias is not None and (bias.dtype != torch.float32 or not bias.is_contiguous()):
         bias = bias.float().contiguous()
+    flags = (L.GEMM_TRANS_A if trans_a else 0) | (L.GEMM_TRANS_B if trans_b else 0)
     args = L.GemmArgs(
         a=a.data_ptr(), b=b.data_ptr(), d=out.data_ptr(), bias=L.ptr(bias), x0=L.ptr(x0), xl=L.ptr(xl),
         aux=L.ptr(aux), m=m, n=n, k=k, lda=a.stride(0), ldb=b.stride(0),
         ld_d=ld_d if ld_d is not None else out.stride(0),
         ld_x=(x0.stride(0) if x0 is not None else 0), rows_per_group=rows_per_group, ld_group=ld_group,
-        beta=beta, in_dtype=in_dt, out_dtype=_dt(out), epilogue=epilogue, pad_=0)
+        beta=beta, in_dtype=in_dt, out_dtype=_dt(out), epilogue=epilogue, flags=flags)
     L.check(L.lib().dmt_gemm_ex(C.byref(args), L.ptr(a_lo), L.ptr(b_lo), L.stream_ptr()), "dmt_gemm")
     return out
 

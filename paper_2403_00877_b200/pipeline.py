@@ -35,6 +35,44 @@ from .plan import ExchangePlan
 from .simnet import CommTrace
 
 
+class PhaseTimers:
+    """CUDA events around pipeline phases, on the stream the kernels run on
+    (the current stream), for the bench's per-kernel roofline."""
+
+    def __init__(self):
+        self.events: dict = {}
+
+    def scope(self, name: str):
+        return _Scope(self, name)
+
+    def reset(self) -> None:
+        self.events = {}
+
+    def ms(self) -> dict:
+        return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.events.items()}
+
+    def count(self, name: str) -> int:
+        return len(self.events.get(name, ()))
+
+
+class _Scope:
+    def __init__(self, timers, name):
+        self.t, self.name = timers, name
+
+    def __enter__(self):
+        if self.t is not None:
+            self.a = torch.cuda.Event(enable_timing=True)
+            self.a.record()
+        return self
+
+    def __exit__(self, *exc):
+        if self.t is not None:
+            b = torch.cuda.Event(enable_timing=True)
+            b.record()
+            self.t.events.setdefault(self.name, []).append((self.a, b))
+        return False
+
+
 @dataclass
 class KJT:
     """A rank's keyed jagged tensor, keys (features) major.
@@ -113,6 +151,10 @@ class SpttEngine:
             else:
                 self.asm_c[r] = self._assemble_table(p.c_blocks(), b["recv_c"], b["out"], p.B)
         self._bwd_ws = {}
+        self.timers: Optional[PhaseTimers] = None
+
+    def _t(self, name: str):
+        return _Scope(self.timers, name)
 
     # ----------------------------------------------------------- tables ----
     def _segments(self, r: int, out: torch.Tensor, with_keys: bool = False) -> K.SegmentTable:
@@ -177,20 +219,24 @@ class SpttEngine:
                 K.kjt_bucketize(kj.lengths, offs, kj.values, p.B, self.slot_feature, so, send_len[r], send_val[r])
             len_splits[r] = p.a_send_length_splits()
             val_splits[r] = p.a_send_value_splits(kj.nnz_per_feature)
-        recv_val_splits = fab.exchange_counts(world, val_splits)
+        with self._t("exchange"):
+            recv_val_splits = fab.exchange_counts(world, val_splits)
         recv_len, recv_val = {}, {}
         for r in self.local:
             recv_len[r] = torch.empty(max(1, p.owner_bags(r)), dtype=torch.int32, device=dev)
             recv_val[r] = torch.empty(max(1, sum(recv_val_splits[r])), dtype=torch.int32, device=dev)
-        fab.alltoallv(world, "a_len", send_len, len_splits, recv_len,
-                      {r: [p.S[r] * p.B] * p.G for r in self.local})
-        fab.alltoallv(world, "a", send_val, val_splits, recv_val, recv_val_splits, self.trace, 4)
+        with self._t("exchange"):
+            fab.alltoallv(world, "a_len", send_len, len_splits, recv_len,
+                          {r: [p.S[r] * p.B] * p.G for r in self.local})
+        with self._t("exchange"):
+            fab.alltoallv(world, "a", send_val, val_splits, recv_val, recv_val_splits, self.trace, 4)
         # step b: lookup (+ fused permute) on every owner
         self._owner = {}
         err = torch.zeros(1, dtype=torch.int32, device=dev) if check_indices else None
         for r in self.local:
             offsets = K.lengths_to_offsets(recv_len[r][: p.owner_bags(r)])
-            K.pooled_lookup_fwd(self.seg_fwd[r], offsets, recv_val[r], err)
+            with self._t("lookup_fwd"):
+                K.pooled_lookup_fwd(self.seg_fwd[r], offsets, recv_val[r], err)
             self._owner[r] = (offsets, recv_val[r], sum(recv_val_splits[r]))
         if err is not None:
             K.raise_lookup_errors(err)
@@ -201,22 +247,25 @@ class SpttEngine:
         recv = {r: self.buf[r]["recv_d"] for r in self.local}
         for g in self._groups(p.group_of):
             self._trace_d(g)
-            fab.alltoallv(g, "d", send, {r: p.d_send_splits(r) for r in g}, recv,
-                          {r: p.d_recv_splits(r) for r in g}, None)
+            with self._t("exchange"):
+                fab.alltoallv(g, "d", send, {r: p.d_send_splits(r) for r in g}, recv,
+                              {r: p.d_recv_splits(r) for r in g}, None)
         # step e: regroup + tower module
         for r in self.local:
             self.asm_e[r].run()
             t = p.tower_of(r)
             if t in self.tm:
-                self.tm[t].forward(self.buf[r]["X"], save=save, out=self.buf[r]["Y"])
+                with self._t("tm_fwd"):
+                    self.tm[t].forward(self.buf[r]["X"], save=save, out=self.buf[r]["Y"])
                 if save:
                     self.buf[r]["tm_saved"] = self.tm[t]._saved
         # step f: per-class all-to-alls, then tower-grouped output
         send = {r: self.buf[r]["Y"].view(-1) for r in self.local}
         recv = {r: self.buf[r]["recv_f"] for r in self.local}
         for g in self._groups(p.class_group_of):
-            fab.alltoallv(g, "f", send, {r: p.f_send_splits(r) for r in g}, recv,
-                          {r: p.f_recv_splits(r) for r in g}, self.trace, self.es)
+            with self._t("exchange"):
+                fab.alltoallv(g, "f", send, {r: p.f_send_splits(r) for r in g}, recv,
+                              {r: p.f_recv_splits(r) for r in g}, self.trace, self.es)
         out = {}
         for r in self.local:
             self.asm_out[r].run()
@@ -228,8 +277,9 @@ class SpttEngine:
         world = list(range(p.G))
         send = {r: self.buf[r]["send_x"] for r in self.local}
         recv = {r: self.buf[r]["recv_c"] for r in self.local}
-        fab.alltoallv(world, "c", send, {r: p.c_send_splits(r) for r in world}, recv,
-                      {r: p.c_recv_splits(r) for r in world}, self.trace, self.es)
+        with self._t("exchange"):
+            fab.alltoallv(world, "c", send, {r: p.c_send_splits(r) for r in world}, recv,
+                          {r: p.c_recv_splits(r) for r in world}, self.trace, self.es)
         out = {}
         for r in self.local:
             self.asm_c[r].run()
@@ -298,8 +348,9 @@ class SpttEngine:
             gsend[r] = gf
             grecv[r] = torch.empty((p.T * p.B, p.O[p.tower_of(r)]), dtype=self.dtype, device=dev)
         for g in self._groups(p.class_group_of):
-            fab.alltoallv(g, "f_bwd", gsend, {r: p.f_recv_splits(r) for r in g}, {r: grecv[r].view(-1) for r in self.local},
-                          {r: p.f_send_splits(r) for r in g})
+            with self._t("exchange"):
+                fab.alltoallv(g, "f_bwd", gsend, {r: p.f_recv_splits(r) for r in g}, {r: grecv[r].view(-1) for r in self.local},
+                              {r: p.f_send_splits(r) for r in g})
         # e^-1: tower module backward (weight grads summed over the tower)
         dX = {}
         tower_grads = {}
@@ -307,7 +358,8 @@ class SpttEngine:
             t = p.tower_of(r)
             if t in self.tm:
                 self.tm[t]._saved = self.buf[r]["tm_saved"]
-                dX[r] = self.tm[t].backward(grecv[r])
+                with self._t("tm_bwd"):
+                    dX[r] = self.tm[t].backward(grecv[r])
                 acc = tower_grads.setdefault(t, {})
                 for k, v in self.tm[t].grads.items():
                     acc[k] = v.clone() if k not in acc else acc[k].add_(v)
@@ -315,7 +367,8 @@ class SpttEngine:
                 dX[r] = grecv[r]
         for t, grads in tower_grads.items():
             group = p.layout.tower_ranks(t, p.topo)
-            fab.all_reduce_(group, grads)
+            with self._t("exchange"):
+                fab.all_reduce_(group, grads)
             self.tm[t].grads = grads
             self.tm[t].sgd_step(tm_lr if tm_lr is not None else lr)
         # d^-1: scatter dX columns back into the step-d receive layout
@@ -331,8 +384,9 @@ class SpttEngine:
             dsend[r] = gd
             drecv[r] = self.buf[r]["grad_x"]
         for g in self._groups(p.group_of):
-            fab.alltoallv(g, "d_bwd", dsend, {r: p.d_recv_splits(r) for r in g}, drecv,
-                          {r: p.d_send_splits(r) for r in g})
+            with self._t("exchange"):
+                fab.alltoallv(g, "d_bwd", dsend, {r: p.d_recv_splits(r) for r in g}, drecv,
+                              {r: p.d_send_splits(r) for r in g})
         self._embedding_update(lr, optimizer, eps)
 
     def _flat_backward(self, grad_out, lr, optimizer, eps):
@@ -348,8 +402,9 @@ class SpttEngine:
                     copies.append((grad_out[r], fb.dst_col + pc.c0, fw, gc, pc.offset, pc.ld, p.B, pc.width))
             K.Copy2DTable(copies, dev).run()
             gsend[r] = gc
-        fab.alltoallv(world, "c_bwd", gsend, {r: p.c_recv_splits(r) for r in world},
-                      {r: self.buf[r]["grad_x"] for r in self.local}, {r: p.c_send_splits(r) for r in world})
+        with self._t("exchange"):
+            fab.alltoallv(world, "c_bwd", gsend, {r: p.c_recv_splits(r) for r in world},
+                          {r: self.buf[r]["grad_x"] for r in self.local}, {r: p.c_send_splits(r) for r in world})
         self._embedding_update(lr, optimizer, eps)
 
     def _embedding_update(self, lr, optimizer, eps):
@@ -358,9 +413,10 @@ class SpttEngine:
         for r in self.local:
             offsets, vals, nnz = self._owner[r]
             ks = self.key_space[r]
-            need = L.lib().dmt_pooled_lookup_bwd_workspace_size(nnz, ks, self.seg_bwd[r].n)
+            need = L.lib().dmt_pooled_lookup_bwd_workspace_size(nnz, ks, self.plan.owner_bags(r))
             ws = self._bwd_ws.get(r)
             if ws is None or ws.numel() < need:
                 ws = torch.empty(max(1, need), dtype=torch.uint8, device=self.device)
                 self._bwd_ws[r] = ws
-            K.pooled_lookup_bwd(self.seg_bwd[r], offsets, vals, nnz, ks, optimizer, lr, eps, ws)
+            with self._t("lookup_bwd"):
+                K.pooled_lookup_bwd(self.seg_bwd[r], offsets, vals, nnz, ks, optimizer, lr, eps, ws)

@@ -55,16 +55,54 @@ class SPTT:
         self.engine = SpttEngine(self.plan, placement, fabric, dtype, self.device, tower_modules=tms, mode=mode,
                                  trace=trace)
         self.tms = tms
+        self.fabric = fabric
+        # flat baseline with the same dense work: one global TM over all
+        # features after the flat all-to-all (what the DMT paper compares to)
+        self.global_tm = None
+        if mode == "flat" and tm is not None and not isinstance(tm, dict) and tm.kind != PASSTHROUGH:
+            ds = {dims[f] for f in feats}
+            n = ds.pop()
+            self.global_tm = TowerModule(tm, len(feats), n, init_tm_weights(tm, len(feats), n, salt=0),
+                                         dtype=dtype, device=self.device)
         self.lr, self.eps = lr, eps
         self.opt = L.OPT_ROWWISE_ADAGRAD if optimizer == "adagrad" else L.OPT_SGD
         if self.opt == L.OPT_ROWWISE_ADAGRAD:
             self.engine.enable_adagrad()
 
+    @property
+    def out_width(self) -> int:
+        if self.global_tm is not None:
+            return self.global_tm.width
+        return self.plan.out_width() if self.plan.feature_towers is not None else self.plan.flat_width()
+
     def forward(self, kjts: dict, save: bool = True) -> dict:
-        return self.engine.forward(kjts, save=save)
+        outs = self.engine.forward(kjts, save=save)
+        if self.global_tm is None:
+            return outs
+        self._gsaved = {}
+        ys = {}
+        for r, o in outs.items():
+            with self.engine._t("tm_fwd"):
+                ys[r] = self.global_tm.forward(o, save=save)
+            self._gsaved[r] = self.global_tm._saved
+        return ys
 
     def backward(self, grads: dict) -> None:
-        self.engine.backward(grads, self.lr, self.opt, self.eps)
+        if self.global_tm is None:
+            self.engine.backward(grads, self.lr, self.opt, self.eps)
+            return
+        dx, acc = {}, {}
+        for r, g in grads.items():
+            self.global_tm._saved = self._gsaved[r]
+            with self.engine._t("tm_bwd"):
+                dx[r] = self.global_tm.backward(g)
+            for k, v in self.global_tm.grads.items():
+                acc[k] = v.clone() if k not in acc else acc[k].add_(v)
+        with self.engine._t("exchange"):
+            self.fabric.all_reduce_(list(range(self.plan.G)), acc)
+        self.global_tm.grads = acc
+        self.global_tm.sgd_step(self.lr)
+        self.engine.backward(dx, self.lr, self.opt, self.eps)
 
     def train_step(self, kjts: dict, grads: dict) -> dict:
         outs = self.forward(kjts, save=True)
@@ -94,6 +132,50 @@ def build_world(G_hosts: int, ranks_per_host: int, hosts_per_tower: int, num_tab
                 f += 1
     plan = {t: TablePlan(scheme, 1 if scheme == "table_wise" else shards_per_table, assignment[t]) for t in tables}
     return topo, layout, shard_tables(tables, plan, topo, layout), assignment
+
+
+def device_world(G_hosts: int, ranks_per_host: int, hosts_per_tower: int, num_tables: int, rows: int, dim: int,
+                 dtype: torch.dtype, local_ranks, seed: int = 0, device=None):
+    """Large synthetic world whose tables are generated directly in HBM (the
+    bench: 26 x 1M x 128 does not need a host copy).  Host-side EmbeddingTable
+    values are zero-stride placeholders; only the shards owned by
+    ``local_ranks`` are materialised, each filled with U(-1, 1) from a
+    per-table seeded device generator."""
+    topo = ClusterTopology(G_hosts, ranks_per_host)
+    W = ranks_per_host * hosts_per_tower
+    layout = TowerLayout(topo.world_size // W, hosts_per_tower)
+    T = layout.num_towers
+    tables = {}
+    for t in range(num_tables):
+        tab = object.__new__(EmbeddingTable)
+        for k, v in (("table_id", t), ("rows", rows), ("dim", dim),
+                     ("values", np.broadcast_to(np.float32(0), (rows, dim)))):
+            object.__setattr__(tab, k, v)
+        tables[t] = tab
+    base, extra = divmod(num_tables, T)
+    assignment, f = {}, 0
+    for t in range(T):
+        for _ in range(base + (1 if t < extra else 0)):
+            assignment[f] = t
+            f += 1
+    from .embedding import Shard
+
+    cursor = [0] * T
+    shards = []
+    for tid in range(num_tables):
+        tw = assignment[tid]
+        ranks = layout.tower_ranks(tw, topo)
+        shards.append(Shard(tid, ranks[cursor[tw] % len(ranks)], "table_wise", (0, rows), (0, dim)))
+        cursor[tw] += 1
+    placement = ShardedEmbedding(tables, shards)
+    device = device or torch.device("cuda")
+    for sid, sh in enumerate(shards):
+        if sh.rank in local_ranks:
+            g = torch.Generator(device=device).manual_seed(seed * 1_000_003 + sh.table_id)
+            w = torch.empty((rows, dim), dtype=torch.float32, device=device).uniform_(-1.0, 1.0, generator=g)
+            placement._dev[(sid, dtype, str(device))] = w.to(dtype).contiguous()
+            del w
+    return topo, layout, placement, assignment
 
 
 def random_kjt(F: int, B: int, rows: int, L_: int, gen: torch.Generator, device) -> KJT:

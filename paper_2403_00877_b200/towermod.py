@@ -246,10 +246,10 @@ class TowerModule:
         if pD:
             g1 = gy[:, :pD]
             if F * N:
-                K.gemm(g1, K.transpose(self.w["w_flat"]), dx)
+                K.gemm(g1, self.w["w_flat"], dx, trans_b=True)
                 first = False
-                self.grads["w_flat"] = K.gemm(K.transpose(g1), K.transpose(x),
-                                              torch.empty((pD, F * N), dtype=f32, device=x.device))
+                self.grads["w_flat"] = K.gemm(g1, x, torch.empty((pD, F * N), dtype=f32, device=x.device),
+                                              trans_a=True, trans_b=True)
             else:
                 self.grads["w_flat"] = torch.zeros_like(self.w["w_flat"], dtype=f32)
             self.grads["b_flat"] = K.column_sum(g1)
@@ -265,11 +265,11 @@ class TowerModule:
             g2v = g2.contiguous().view(rows * F, cD)
             xv = x.view(rows * F, N)
             dxv = dx.view(rows * F, N)
-            K.gemm(g2v, K.transpose(self.w["w_feat"]), dxv, epilogue=L.EPI_NONE if first else L.EPI_ACC,
-                   beta=0.0 if first else 1.0)
+            K.gemm(g2v, self.w["w_feat"], dxv, epilogue=L.EPI_NONE if first else L.EPI_ACC,
+                   beta=0.0 if first else 1.0, trans_b=True)
             first = False
-            self.grads["w_feat"] = K.gemm(K.transpose(g2v), K.transpose(xv),
-                                          torch.empty((cD, N), dtype=f32, device=x.device))
+            self.grads["w_feat"] = K.gemm(g2v, xv, torch.empty((cD, N), dtype=f32, device=x.device),
+                                          trans_a=True, trans_b=True)
             self.grads["b_feat"] = K.column_sum(g2v)
         else:
             self.grads["w_feat"] = torch.zeros_like(self.w["w_feat"], dtype=f32)
@@ -283,20 +283,20 @@ class TowerModule:
         x0 = xs[0]
         rows, M = x0.shape
         f32 = torch.float32
-        self.grads["w_proj"] = K.gemm(K.transpose(gy), K.transpose(xs[-1]),
-                                      torch.empty(self.w["w_proj"].shape, dtype=f32, device=x0.device))
+        self.grads["w_proj"] = K.gemm(gy, xs[-1], torch.empty(self.w["w_proj"].shape, dtype=f32, device=x0.device),
+                                      trans_a=True, trans_b=True)
         self.grads["b_proj"] = K.column_sum(gy)
         g = torch.empty((rows, M), dtype=self.dtype, device=x0.device)
-        K.gemm(gy, K.transpose(self.w["w_proj"]), g)
+        K.gemm(gy, self.w["w_proj"], g, trans_b=True)
         dx0 = torch.zeros((rows, M), dtype=f32, device=x0.device)
         gu = torch.empty_like(g)
         for layer in range(self.cfg.cross_layers - 1, -1, -1):
             K.cross_bwd_pointwise(g, x0, us[layer], gu, dx0)
-            self.grads[f"w{layer}"] = K.gemm(K.transpose(gu), K.transpose(xs[layer]),
-                                             torch.empty((M, M), dtype=f32, device=x0.device))
+            self.grads[f"w{layer}"] = K.gemm(gu, xs[layer], torch.empty((M, M), dtype=f32, device=x0.device),
+                                             trans_a=True, trans_b=True)
             self.grads[f"b{layer}"] = K.column_sum(gu)
             # g <- gu @ W + g   (in-place accumulate epilogue)
-            K.gemm(gu, K.transpose(self.w[f"w{layer}"]), g, epilogue=L.EPI_ACC, beta=1.0)
+            K.gemm(gu, self.w[f"w{layer}"], g, epilogue=L.EPI_ACC, beta=1.0, trans_b=True)
         # dX = dx0 + g
         dx = torch.empty_like(g)
         tmp = K.convert(dx0, self.dtype)

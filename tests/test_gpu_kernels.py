@@ -192,3 +192,23 @@ def test_gemm_grouped_rows_output():
     want = (x.double().view(rows, F, N) @ w.double().T + bias.double()).reshape(rows, F * cD)
     assert torch.allclose(y[:, pD:].double(), want, rtol=1e-5, atol=1e-5)
     assert (y[:, :pD] == 0).all()
+
+
+@pytest.mark.parametrize("ta,tb", [(True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("m,n,k", [(128, 128, 64), (300, 200, 136), (3328 // 4, 512, 1024), (70, 90, 8)])
+def test_gemm_mn_major_operands(ta, tb, dt, m, n, k):
+    """A / B read MN-major straight from (k, m) / (k, n) storage -- no transpose."""
+    from paper_2403_00877_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = torch.randn(m, k, device="cuda", generator=g).to(dt)
+    Bm = torch.randn(n, k, device="cuda", generator=g).to(dt)
+    a = A.t().contiguous() if ta else A
+    b = Bm.t().contiguous() if tb else Bm
+    out = torch.empty(m, n, device="cuda", dtype=torch.float32)
+    K.gemm(a, b, out, trans_a=ta, trans_b=tb)
+    want = A.double() @ Bm.double().T
+    tol = 1e-5 if dt == torch.float32 else 1e-2
+    scale = (A.double().abs() @ Bm.double().abs().T).max().item()
+    assert (out.double() - want).abs().max().item() <= tol * scale

@@ -1,0 +1,194 @@
+"""GPU parity of the backward path: fused embedding-bag backward + optimizers,
+tower-module backward, and a full SPTT train step (loopback ranks) against the
+oracle's restatement (oracle/backward.py)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+
+
+def dev():
+    return torch.device("cuda")
+
+
+def _bwd_case(rng, rows, width, nbags, maxlen, mode, hot=False):
+    lens = np.ones(nbags, np.int64) if mode == "none" else rng.integers(0, maxlen + 1, size=nbags)
+    if hot:  # power-law-ish: many repeats of a few rows
+        idx = (rng.zipf(1.3, size=int(lens.sum())) - 1) % rows
+    else:
+        idx = rng.integers(0, rows, size=int(lens.sum()))
+    g = rng.normal(size=(nbags, width)).astype(np.float32)
+    return lens, idx, g
+
+
+@pytest.mark.parametrize("opt", ["sgd", "adagrad"])
+@pytest.mark.parametrize("mode", ["sum", "mean", "none"])
+@pytest.mark.parametrize("hot", [False, True])
+@pytest.mark.parametrize("width", [4, 64, 128, 200])
+def test_embedding_backward_fused_optimizer(opt, mode, hot, width):
+    from paper_2403_00877_b200 import _lib as L
+    from paper_2403_00877_b200 import kernels as K
+
+    rng = np.random.default_rng(width + (7 if hot else 0))
+    rows = 500
+    table = rng.uniform(-1, 1, (rows, width)).astype(np.float32)
+    lens, idx, g = _bwd_case(rng, rows, width, 300, 12, mode, hot)
+    W = torch.from_numpy(table.copy()).to(dev())
+    G = torch.from_numpy(g).to(dev())
+    state = torch.full((rows,), 0.1, dtype=torch.float32, device=dev())
+    offs = K.lengths_to_offsets(torch.from_numpy(lens.astype(np.int32)).to(dev()))
+    I = torch.from_numpy(idx.astype(np.int32)).to(dev())
+    seg = K.Segment(weights=W, out=G, out_offset=0, out_ld=width, bag_begin=0, nbags=len(lens),
+                    pooling=L.POOL_CODE[mode], state=state if opt == "adagrad" else None)
+    ws = K.pooled_lookup_bwd_workspace(int(lens.sum()), rows, len(lens), dev())
+    K.pooled_lookup_bwd(K.SegmentTable([seg], dev()), offs, I, int(lens.sum()), rows,
+                        L.OPT_ROWWISE_ADAGRAD if opt == "adagrad" else L.OPT_SGD, 0.05, 1e-8, ws)
+    uniq, grads = oracle.embedding_row_grads(rows, lens, idx, g.astype(np.float64), mode)
+    if opt == "sgd":
+        want = oracle.apply_sgd(table, uniq, grads, 0.05)
+    else:
+        want, want_s = oracle.apply_rowwise_adagrad(table, np.full(rows, 0.1), uniq, grads, 0.05, 1e-8)
+        np.testing.assert_allclose(state.double().cpu().numpy(), want_s, rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(W.double().cpu().numpy(), want, rtol=1e-5, atol=1e-5)
+
+
+def test_embedding_backward_is_deterministic():
+    from paper_2403_00877_b200 import _lib as L
+    from paper_2403_00877_b200 import kernels as K
+
+    rng = np.random.default_rng(1)
+    rows, width = 64, 128
+    lens, idx, g = _bwd_case(rng, rows, width, 4000, 30, "sum", hot=True)
+    outs = []
+    for _ in range(3):
+        W = torch.zeros((rows, width), dtype=torch.float32, device=dev())
+        offs = K.lengths_to_offsets(torch.from_numpy(lens.astype(np.int32)).to(dev()))
+        seg = K.Segment(weights=W, out=torch.from_numpy(g).to(dev()), out_offset=0, out_ld=width, bag_begin=0,
+                        nbags=len(lens), pooling=L.POOL_SUM)
+        ws = K.pooled_lookup_bwd_workspace(int(lens.sum()), rows, len(lens), dev())
+        K.pooled_lookup_bwd(K.SegmentTable([seg], dev()), offs, torch.from_numpy(idx.astype(np.int32)).to(dev()),
+                            int(lens.sum()), rows, L.OPT_SGD, 1.0, 0.0, ws)
+        outs.append(W.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+
+
+def _tm_objects(kind, F, N, dt, seed=0):
+    import paper_2403_00877_b200 as P
+
+    if kind == "dlrm":
+        cfg = P.TMConfig(kind="dlrm", out_dim=16, per_feature_outputs=2, flat_outputs=1, seed=seed)
+        ocfg = {"kind": "dlrm", "out_dim": 16, "per_feature_outputs": 2, "flat_outputs": 1, "cross_layers": 3,
+                "seed": seed}
+    else:
+        cfg = P.TMConfig(kind="dcn", out_dim=16, cross_layers=3, seed=seed)
+        ocfg = {"kind": "dcn", "out_dim": 16, "per_feature_outputs": 1, "flat_outputs": 0, "cross_layers": 3,
+                "seed": seed}
+    w = P.init_tm_weights(cfg, F, N, salt=1)
+    ow = oracle.init_tm_weights(ocfg, F, N, salt=1)
+    return P.TowerModule(cfg, F, N, w, dtype=dt), ocfg, ow
+
+
+@pytest.mark.parametrize("kind", ["dlrm", "dcn"])
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+def test_tower_module_backward_vs_oracle(kind, dt):
+    F, N, rows = 6, 32, 300
+    tm, ocfg, ow = _tm_objects(kind, F, N, dt)
+    rng = np.random.default_rng(4)
+    x = rng.normal(size=(rows, F, N)) * 0.5
+    if dt == torch.bfloat16:
+        x = oracle.bf16_round(x.astype(np.float32)).astype(np.float64)
+    xt = torch.from_numpy(x.reshape(rows, F * N)).to(dev(), dt)
+    y = tm.forward(xt, save=True)
+    want_y = oracle.tm_forward(x, ocfg, ow)
+    tol = 1e-5 if dt == torch.float32 else 3e-2
+    scale = max(1.0, np.abs(want_y).max())
+    assert np.abs(y.double().cpu().numpy() - want_y).max() <= tol * scale
+    g = rng.normal(size=want_y.shape)
+    if dt == torch.bfloat16:
+        g = oracle.bf16_round(g.astype(np.float32)).astype(np.float64)
+    dx = tm.backward(torch.from_numpy(g).to(dev(), dt))
+    want_dx, want_dw = oracle.tm_backward(x, ocfg, ow, g)
+    sdx = max(1.0, np.abs(want_dx).max())
+    assert np.abs(dx.double().cpu().numpy().reshape(rows, F, N) - want_dx).max() <= tol * sdx * 4
+    if kind == "dlrm":
+        pairs = [(k, want_dw[k]) for k in ("w_flat", "b_flat", "w_feat", "b_feat")]
+    else:
+        pairs = [("w_proj", want_dw["w_proj"]), ("b_proj", want_dw["b_proj"])]
+        for i, (gw, gb) in enumerate(want_dw["cross"]):
+            pairs += [(f"w{i}", gw), (f"b{i}", gb)]
+    for k, want in pairs:
+        got = tm.grads[k].double().cpu().numpy()
+        s = max(1.0, np.abs(want).max())
+        assert np.abs(got - want).max() <= tol * s * 4, k
+
+
+@pytest.mark.parametrize("hosts,rph,kind", [(2, 2, "dlrm"), (2, 4, "dcn"), (4, 2, "dcn"), (1, 1, "dcn")])
+def test_sptt_train_step_loopback_vs_oracle(hosts, rph, kind):
+    """Full step on G simulated ranks: outputs, then every table row after SGD."""
+    import paper_2403_00877_b200 as P
+    from paper_2403_00877_b200.fabric import LoopbackFabric
+    from paper_2403_00877_b200.pipeline import KJT
+    from paper_2403_00877_b200.sptt import SPTT, build_world
+
+    F, rows, N, B = 8, 60, 16, 5
+    topo, layout, placement, assignment = build_world(hosts, rph, 1, F, rows, N, seed=2)
+    G, T = topo.world_size, layout.num_towers
+    pooling = {f: ("mean" if f % 3 == 0 else "sum") for f in range(F)}
+    if kind == "dlrm":
+        cfg = P.TMConfig(kind="dlrm", out_dim=8, per_feature_outputs=1, flat_outputs=1, seed=1)
+    else:
+        cfg = P.TMConfig(kind="dcn", out_dim=8, cross_layers=2, seed=1)
+    ocfg = {"kind": cfg.kind, "out_dim": 8, "per_feature_outputs": cfg.per_feature_outputs,
+            "flat_outputs": cfg.flat_outputs, "cross_layers": cfg.cross_layers, "seed": 1}
+    before = {t: placement.tables[t].values.astype(np.float64).copy() for t in range(F)}
+    lr = 0.05
+    model = SPTT(topo, layout, placement, assignment, pooling, B, LoopbackFabric(G, dev()), tm=cfg,
+                 dtype=torch.float32, lr=lr)
+    rng = np.random.default_rng(11)
+    lens = rng.integers(0, 5, size=(G, F, B)).astype(np.int32)
+    vals = rng.integers(0, rows, size=int(lens.sum())).astype(np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens.reshape(-1))])
+    kjts = {}
+    for r in range(G):
+        seg = vals[offs[r * F * B]:offs[(r + 1) * F * B]]
+        kjts[r] = KJT(torch.from_numpy(lens[r].reshape(-1)).to(dev()), torch.from_numpy(seg.astype(np.int32)).to(dev()),
+                      [int(lens[r, f].sum()) for f in range(F)], B)
+    O = model.plan.out_width()
+    grads = {r: torch.from_numpy(rng.normal(size=(B, O)).astype(np.float32)).to(dev()) for r in range(G)}
+    outs = model.train_step(kjts, grads)
+    torch.cuda.synchronize()
+
+    shards = [(s.table_id, s.rank, s.scheme, s.row_range, s.col_range) for s in placement.shards]
+    flat, _, _, _ = oracle.baseline_forward(lens, vals, list(range(F)), pooling, before, shards,
+                                            oracle.OTopo(hosts, rph))
+    by_tower = {t: [f for f in range(F) if assignment[f] == t] for t in range(T)}
+    tw = {t: oracle.init_tm_weights(ocfg, len(by_tower[t]), N, salt=t) for t in range(T)}
+    expect = {t: before[t].copy() for t in range(F)}
+    tw_grads = {t: None for t in range(T)}
+    for r in range(G):
+        g_r = grads[r].double().cpu().numpy()
+        col = 0
+        for t in range(T):
+            fs = by_tower[t]
+            x = flat[r][:, fs[0] * N:(fs[-1] + 1) * N].reshape(B, len(fs), N)
+            ow_ = oracle.tm_output_width(ocfg, len(fs), N)
+            y = oracle.tm_forward(x, ocfg, tw[t])
+            np.testing.assert_allclose(outs[r][:, col:col + ow_].double().cpu().numpy(), y, rtol=1e-5, atol=1e-5)
+            dx, _ = oracle.tm_backward(x, ocfg, tw[t], g_r[:, col:col + ow_])
+            col += ow_
+            for i, f in enumerate(fs):
+                base = (r * F + f) * B
+                for b in range(B):
+                    n = offs[base + b + 1] - offs[base + b]
+                    for k in range(offs[base + b], offs[base + b + 1]):
+                        scale = 1.0 / n if pooling[f] == "mean" else 1.0
+                        expect[f][vals[k]] -= lr * scale * dx[b, i]
+    for sid, sh in enumerate(placement.shards):
+        got = model.engine.weights[sid].double().cpu().numpy()
+        np.testing.assert_allclose(got, expect[sh.table_id], rtol=1e-4, atol=2e-5)
