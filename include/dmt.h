@@ -184,13 +184,26 @@ int dmt_batched_copy2d(const dmt_copy2d* copies, int32_t n, int32_t elem_bytes, 
  *   DMT_EPI_ACC  : v = acc + beta*C[m, n] (C = d)
  * Output row m goes to d + (m / rows_per_group)*ld_group + (m % rows_per_group)*ld_d,
  * so the per-feature DLRM projection can write straight into the tower output. */
-enum dmt_epilogue { DMT_EPI_NONE = 0, DMT_EPI_BIAS = 1, DMT_EPI_CROSS = 2, DMT_EPI_ACC = 3 };
+enum dmt_epilogue {
+  DMT_EPI_NONE = 0,
+  DMT_EPI_BIAS = 1,
+  DMT_EPI_CROSS = 2,
+  DMT_EPI_ACC = 3,
+  /* DCN backward, one layer (towermod.py:132-139 differentiated):
+   *   g  = acc + beta*C            -> d      (dL/dx_{l+1})
+   *   gu = g * x0                  -> aux    (dL/du_l, A operand of the next GEMMs)
+   *   dx0 (+)= g * u_l             -> aux2   (fp32, accumulated if FLAG_AUX2_ACCUM)
+   * with x0 = args.x0 and u_l = args.xl. */
+  DMT_EPI_DCN_BWD = 4,
+  /* last DCN layer: d = acc + beta*C + aux2 (fp32 dx0)  ->  dX of the tower */
+  DMT_EPI_DCN_FINAL = 5
+};
 
 /* dmt_gemm_args.flags: operand stored transposed (MN-major).  TRANS_A: `a`
  * holds A^T as a [k, m] matrix with row stride lda (m contiguous); TRANS_B:
  * `b` holds B^T as [k, n] with row stride ldb.  Read straight by TMA, no
  * transpose pass (dW = G^T X, dX = G W). */
-enum dmt_gemm_flags { DMT_GEMM_TRANS_A = 1, DMT_GEMM_TRANS_B = 2 };
+enum dmt_gemm_flags { DMT_GEMM_TRANS_A = 1, DMT_GEMM_TRANS_B = 2, DMT_GEMM_AUX2_ACCUM = 4 };
 
 typedef struct dmt_gemm_args {
   const void* a;   /* [m, k] row stride lda */
@@ -199,7 +212,9 @@ typedef struct dmt_gemm_args {
   const float* bias;
   const void* x0;  /* CROSS: [m, n] row stride ld_x */
   const void* xl;
-  void* aux;       /* CROSS: u = acc + bias, row stride ld_x (may be NULL) */
+  void* aux;       /* CROSS: u = acc + bias, row stride ld_x (may be NULL); DCN_BWD: gu */
+  const void* c;   /* ACC / DCN_*: accumulate source C[m, n] (row stride ld_d; NULL = d) */
+  float* aux2;     /* DCN_*: fp32 dx0, row stride ld_x */
   int64_t m, n, k;
   int64_t lda, ldb, ld_d, ld_x;
   int64_t rows_per_group, ld_group;

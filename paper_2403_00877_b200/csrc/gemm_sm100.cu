@@ -12,9 +12,9 @@
 //                 mbarrier full/empty ring of STAGES operand slots
 //   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer; commits
 //                 free smem slots and publish finished accumulators
-//   warps 2..5  : epilogue -- tcgen05.ld TMEM -> registers, bias / crossnet
-//                 gate / accumulate, convert, store; warp w owns TMEM lanes
-//                 32*(w%4) .. +31 (one output row per thread)
+//   warps 2..9  : epilogue -- tcgen05.ld TMEM -> registers, bias / crossnet
+//                 gate / DCN-backward / accumulate, convert, store; warp w owns TMEM lanes
+//                 32*(w%4) .. +31 (one output row per thread) and half the columns
 // Two TMEM accumulators (2 x BN fp32 columns) let the epilogue of tile i
 // overlap the MMAs of tile i+1.
 //
@@ -30,7 +30,8 @@
 namespace dmt {
 namespace gemm {
 
-constexpr int kThreads = 192;  // 6 warps
+constexpr int kEpiWarps = 8;   // two warps per TMEM lane quarter, each owns half the columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kBlockM = 128;
 constexpr int kAtomBytes = 128;  // one SWIZZLE_128B row = BLOCK_K bytes per stage
 constexpr int kUmmaKBytes = 32;  // K bytes consumed by one tcgen05.mma (16 x bf16 / 8 x tf32)
@@ -173,12 +174,16 @@ struct Params {
   const void* x0;
   const void* xl;
   void* aux;
+  const void* c;
+  float* aux2;
   float beta;
+  int aux2_accum;
   int out_dtype;
   int in_dtype;
   int epilogue;
   int vec_store;
   int vec_x;
+  int coalesced;
 };
 
 // 32 consecutive elements of one row <-> 32 fp32 registers.  The vector forms
@@ -229,6 +234,172 @@ __device__ __forceinline__ void store32s(TO* __restrict__ p, const float* v, int
     if (i < n) p[i] = from_f<TO>(v[i]);
 }
 
+// 8 consecutive elements (16 B for 16-bit types, 32 B for fp32) <-> 8 floats.
+template <typename T>
+__device__ __forceinline__ void load8(const T* __restrict__ p, float* v) {
+  if constexpr (sizeof(T) == 4) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+    uint4 x = *reinterpret_cast<const uint4*>(p);
+    const T* h = reinterpret_cast<const T*>(&x);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = to_f<T>(h[j]);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void store8(T* __restrict__ p, const float* v) {
+  if constexpr (sizeof(T) == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+    uint4 x;
+    T* h = reinterpret_cast<T*>(&x);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[j] = from_f<T>(v[j]);
+    *reinterpret_cast<uint4*>(p) = x;
+  }
+}
+
+// Epilogue math for 8 columns of one row (coalesced path: 4 lanes per row).
+template <typename TIN, typename TO>
+__device__ __forceinline__ void epi8(const Params& p, int64_t row, int64_t col, float* v) {
+  if (p.epilogue == DMT_EPI_BIAS || p.epilogue == DMT_EPI_CROSS) {
+    float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + col));
+    float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + col + 4));
+    v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+    v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+  }
+  const int64_t xo = row * p.ld_x + col;
+  if (p.epilogue == DMT_EPI_CROSS) {
+    float a[8], b[8];
+    load8<TIN>(reinterpret_cast<const TIN*>(p.x0) + xo, a);
+    load8<TIN>(reinterpret_cast<const TIN*>(p.xl) + xo, b);
+    if (p.aux) store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = a[j] * v[j] + b[j];
+  } else if (p.epilogue == DMT_EPI_ACC || p.epilogue == DMT_EPI_DCN_BWD || p.epilogue == DMT_EPI_DCN_FINAL) {
+    if (p.beta != 0.f) {
+      float c[8];
+      load8<TO>(reinterpret_cast<const TO*>(p.c) + row * p.ld_d + col, c);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += p.beta * c[j];
+    }
+    if (p.epilogue == DMT_EPI_DCN_FINAL) {
+      float d[8];
+      load8<float>(p.aux2 + xo, d);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += d[j];
+    } else if (p.epilogue == DMT_EPI_DCN_BWD) {
+      float x0[8], u[8], d[8];
+      load8<TIN>(reinterpret_cast<const TIN*>(p.x0) + xo, x0);
+      load8<TIN>(reinterpret_cast<const TIN*>(p.xl) + xo, u);
+      if (p.aux2_accum) load8<float>(p.aux2 + xo, d);
+      else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        x0[j] *= v[j];          // gu = g * x0
+        d[j] += v[j] * u[j];    // dx0 += g * u
+      }
+      store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, x0);
+      store8<float>(p.aux2 + xo, d);
+    }
+  }
+  TO* drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
+  store8<TO>(drow + col, v);
+}
+
+// Raw (unconverted) epilogue inputs of one 8-column row piece, so two pieces'
+// loads can be in flight before either is consumed (memory-level parallelism).
+template <typename TIN, typename TO>
+struct EpiIn {
+  using RI = typename std::conditional<sizeof(TIN) == 4, float4, uint4>::type;
+  using RO = typename std::conditional<sizeof(TO) == 4, float4, uint4>::type;
+  RI x0[sizeof(TIN) == 4 ? 2 : 1], u[sizeof(TIN) == 4 ? 2 : 1];
+  RO c[sizeof(TO) == 4 ? 2 : 1];
+  float4 d[2];
+};
+
+template <typename R, typename T, int N>
+__device__ __forceinline__ void rawld(const T* p, R (&r)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) r[i] = reinterpret_cast<const R*>(p)[i];
+}
+template <typename R, typename T, int N>
+__device__ __forceinline__ void rawcvt(const R (&r)[N], float* v) {
+  load8<T>(reinterpret_cast<const T*>(&r[0]), v);
+}
+
+template <typename TIN, typename TO>
+__device__ __forceinline__ void epi_load(const Params& p, int64_t row, int64_t col, EpiIn<TIN, TO>& in) {
+  const int64_t xo = row * p.ld_x + col;
+  const int e = p.epilogue;
+  if (e == DMT_EPI_CROSS || e == DMT_EPI_DCN_BWD) {
+    rawld(reinterpret_cast<const TIN*>(p.x0) + xo, in.x0);
+    rawld(reinterpret_cast<const TIN*>(p.xl) + xo, in.u);
+  }
+  if ((e == DMT_EPI_ACC || e == DMT_EPI_DCN_BWD || e == DMT_EPI_DCN_FINAL) && p.beta != 0.f)
+    rawld(reinterpret_cast<const TO*>(p.c) + row * p.ld_d + col, in.c);
+  if (e == DMT_EPI_DCN_FINAL || (e == DMT_EPI_DCN_BWD && p.aux2_accum)) rawld(p.aux2 + xo, in.d);
+}
+
+template <typename TIN, typename TO>
+__device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t col, float* v,
+                                           const EpiIn<TIN, TO>& in) {
+  const int e = p.epilogue;
+  if (e == DMT_EPI_BIAS || e == DMT_EPI_CROSS) {
+    float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + col));
+    float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + col + 4));
+    v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+    v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+  }
+  const int64_t xo = row * p.ld_x + col;
+  if (e == DMT_EPI_CROSS) {
+    float a[8], b[8];
+    rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.x0, a);
+    rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.u, b);
+    if (p.aux) store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = a[j] * v[j] + b[j];
+  } else if (e == DMT_EPI_ACC || e == DMT_EPI_DCN_BWD || e == DMT_EPI_DCN_FINAL) {
+    if (p.beta != 0.f) {
+      float c[8];
+      rawcvt<typename EpiIn<TIN, TO>::RO, TO>(in.c, c);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += p.beta * c[j];
+    }
+    if (e == DMT_EPI_DCN_FINAL) {
+      float d[8];
+      rawcvt<float4, float>(in.d, d);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += d[j];
+    } else if (e == DMT_EPI_DCN_BWD) {
+      float x0[8], u[8], d[8];
+      rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.x0, x0);
+      rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.u, u);
+      if (p.aux2_accum) rawcvt<float4, float>(in.d, d);
+      else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        x0[j] *= v[j];
+        d[j] += v[j] * u[j];
+      }
+      store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, x0);
+      store8<float>(p.aux2 + xo, d);
+    }
+  }
+  TO* drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
+  store8<TO>(drow + col, v);
+}
+
+constexpr int kStileFloats = 32 * 33;  // per-warp padded 32x32 fp32 staging tile
+
 // BN: tile N (64/128/256); NOPS: 1 (plain) or 3 (3xTF32); KIND: 0 f16-family, 1 tf32
 template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -248,6 +419,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stile_all = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tiles_m = ceil_div(p.m, kBlockM), tiles_n = ceil_div(p.n, BN);
@@ -264,7 +436,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[s], kEpiWarps);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -347,7 +519,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    const int q = warp & 3;                       // TMEM lane quarter accessible to this warp
+    const int half = (warp - 2) / 4;              // which half of the tile's columns
+    constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -361,14 +535,44 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       TO* drow = nullptr;
       if (row_ok)
         drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
+      float* stile = stile_all + (warp - 2) * kStileFloats;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = half * kColsPerWarp; c < (half + 1) * kColsPerWarp; c += 32) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), v);
         const int64_t col = n0 + c;
         const int64_t rem = p.n - col;
         const int ncols = rem <= 0 ? 0 : (rem < 32 ? (int)rem : 32);
-        if (!row_ok || ncols == 0) continue;
+        if (ncols == 0) continue;  // warp-uniform
+        if (ncols == 32 && p.coalesced) {
+          // stage the 32x32 chunk (thread = row) through a padded smem tile,
+          // then 4 lanes per row: every global access of the warp covers 8
+          // rows x 64-128 contiguous bytes instead of 32 scattered rows.
+#pragma unroll
+          for (int i = 0; i < 32; ++i) stile[lane * 33 + i] = v[i];
+          __syncwarp();
+          const int c8 = (lane & 3) * 8;
+#pragma unroll 1
+          for (int it = 0; it < 4; it += 2) {
+            // two 8-row slabs per pass: both slabs' inputs are loaded before
+            // either is consumed
+            const int rl0 = it * 8 + (lane >> 2), rl1 = rl0 + 8;
+            const int64_t r0 = m0 + q * 32 + rl0, r1 = r0 + 8;
+            EpiIn<TIN, TO> in0, in1;
+            if (r0 < p.m) epi_load<TIN, TO>(p, r0, col + c8, in0);
+            if (r1 < p.m) epi_load<TIN, TO>(p, r1, col + c8, in1);
+            float a[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[j] = stile[rl0 * 33 + c8 + j];
+            if (r0 < p.m) epi_finish<TIN, TO>(p, r0, col + c8, a, in0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[j] = stile[rl1 * 33 + c8 + j];
+            if (r1 < p.m) epi_finish<TIN, TO>(p, r1, col + c8, a, in1);
+          }
+          __syncwarp();
+          continue;
+        }
+        if (!row_ok) continue;
         const bool full = ncols == 32;
         if (p.epilogue == DMT_EPI_BIAS || p.epilogue == DMT_EPI_CROSS) {
           if (full) {
@@ -404,12 +608,51 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += t[i];
           }
-        } else if (p.epilogue == DMT_EPI_ACC) {
-          float t[32];
-          if (full && p.vec_store) load32v<TO>(drow + col, t);
-          else load32s<TO>(drow + col, t, ncols);
+        } else if (p.epilogue == DMT_EPI_ACC || p.epilogue == DMT_EPI_DCN_BWD || p.epilogue == DMT_EPI_DCN_FINAL) {
+          if (p.beta != 0.f) {
+            const TO* cp = reinterpret_cast<const TO*>(p.c) + row * p.ld_d + col;
+            float t[32];
+            if (full && p.vec_store) load32v<TO>(cp, t);
+            else load32s<TO>(cp, t, ncols);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += p.beta * t[i];
+            for (int i = 0; i < 32; ++i) v[i] += p.beta * t[i];
+          }
+          if (p.epilogue != DMT_EPI_ACC) {
+            float* dxp = p.aux2 + row * p.ld_x + col;
+            const bool vx = full && p.vec_x;
+            if (p.epilogue == DMT_EPI_DCN_FINAL) {
+              float t[32];
+              if (vx) load32v<float>(dxp, t);
+              else load32s<float>(dxp, t, ncols);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += t[i];
+            } else {
+              // g = v; gu = g * x0 -> aux; dx0 (+)= g * u -> aux2
+              const TIN* x0p = reinterpret_cast<const TIN*>(p.x0) + row * p.ld_x + col;
+              const TIN* up = reinterpret_cast<const TIN*>(p.xl) + row * p.ld_x + col;
+              TIN* gup = reinterpret_cast<TIN*>(p.aux) + row * p.ld_x + col;
+              float t[32], w[32];
+              if (vx) load32v<TIN>(x0p, t);
+              else load32s<TIN>(x0p, t, ncols);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) w[i] = v[i] * t[i];
+              if (vx) store32v<TIN>(gup, w);
+              else store32s<TIN>(gup, w, ncols);
+              if (vx) load32v<TIN>(up, t);
+              else load32s<TIN>(up, t, ncols);
+              if (p.aux2_accum) {
+                if (vx) load32v<float>(dxp, w);
+                else load32s<float>(dxp, w, ncols);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) w[i] = 0.f;
+              }
+#pragma unroll
+              for (int i = 0; i < 32; ++i) w[i] += v[i] * t[i];
+              if (vx) store32v<float>(dxp, w);
+              else store32s<float>(dxp, w, ncols);
+            }
+          }
         }
         if (full && p.vec_store) store32v<TO>(drow + col, v);
         else store32s<TO>(drow + col, v, ncols);
@@ -474,7 +717,8 @@ template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, boo
 static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cudaStream_t s) {
   constexpr int NSETS = (NOPS == 3) ? 2 : 1;
   constexpr int STAGE_BYTES = NSETS * (kBlockM + BN) * kAtomBytes;
-  constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                          (size_t)kEpiWarps * kStileFloats * 4 /*epilogue staging*/;
   static_assert(SMEM <= 232448, "smem");
   CUtensorMap ma, mb, mal, mbl;
   if (!make_map(&ma, a->a, a->m, a->k, a->lda, a->in_dtype, kBlockM, AMN)) return DMT_ERR_CUDA;
@@ -492,12 +736,18 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   p.rows_per_group = a->rows_per_group > 0 ? a->rows_per_group : a->m + 1;
   p.ld_group = a->ld_group;
   p.d = a->d; p.bias = a->bias; p.x0 = a->x0; p.xl = a->xl; p.aux = a->aux;
+  p.c = a->c ? a->c : a->d;
+  p.aux2 = a->aux2;
+  p.aux2_accum = (a->flags & DMT_GEMM_AUX2_ACCUM) != 0;
   p.beta = a->beta; p.out_dtype = a->out_dtype; p.in_dtype = a->in_dtype; p.epilogue = a->epilogue;
   size_t eo = dtype_size(a->out_dtype);
   p.vec_store = ((uintptr_t)a->d % 16 == 0) && ((a->ld_d * eo) % 16 == 0) && ((a->ld_group * eo) % 16 == 0);
   size_t ei = dtype_size(a->in_dtype);
   p.vec_x = ((uintptr_t)a->x0 % 16 == 0) && ((uintptr_t)a->xl % 16 == 0) && ((uintptr_t)a->aux % 16 == 0) &&
-            ((a->ld_x * ei) % 16 == 0);
+            ((uintptr_t)a->aux2 % 16 == 0) && ((a->ld_x * ei) % 16 == 0) && ((a->ld_x * 4) % 16 == 0);
+  p.vec_store = p.vec_store && ((uintptr_t)p.c % 16 == 0);
+  const bool needs_x = a->epilogue == DMT_EPI_CROSS || a->epilogue == DMT_EPI_DCN_BWD || a->epilogue == DMT_EPI_DCN_FINAL;
+  p.coalesced = p.vec_store && (!needs_x || p.vec_x);
   if (a->bias && ((uintptr_t)a->bias % 16)) return DMT_ERR_UNSUPPORTED;
   auto kern = gemm_kernel<BN, NOPS, KIND, STAGES, TIN, TO, AMN, BMN>;
   static bool attr_set = false;
@@ -576,6 +826,11 @@ int dmt_gemm_ex(const dmt_gemm_args* args, const void* a_lo, const void* b_lo, d
     return DMT_ERR_UNSUPPORTED;
   if ((a->epilogue == DMT_EPI_BIAS || a->epilogue == DMT_EPI_CROSS) && !a->bias) return DMT_ERR_DOMAIN;
   if (a->epilogue == DMT_EPI_CROSS && (!a->x0 || !a->xl)) return DMT_ERR_DOMAIN;
+  if (a->epilogue == DMT_EPI_DCN_BWD && (!a->x0 || !a->xl || !a->aux || !a->aux2)) return DMT_ERR_DOMAIN;
+  if (a->epilogue == DMT_EPI_DCN_FINAL && !a->aux2) return DMT_ERR_DOMAIN;
+  if ((a->epilogue == DMT_EPI_DCN_BWD || a->epilogue == DMT_EPI_DCN_FINAL) && a->out_dtype != a->in_dtype)
+    return DMT_ERR_UNSUPPORTED;
+  if (a->epilogue > DMT_EPI_DCN_FINAL || a->epilogue < 0) return DMT_ERR_DOMAIN;
   cudaStream_t s = (cudaStream_t)stream;
   switch (a->in_dtype) {
     case DMT_BF16: return gemm::dispatch_out<__nv_bfloat16>(a, nullptr, nullptr, s);

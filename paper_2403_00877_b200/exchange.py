@@ -249,6 +249,8 @@ class _MixedEngine(SpttEngine):
             t = plan.tower_of(r)
             if t in tms:
                 self.buf[r]["Y"] = torch.empty((plan.T * plan.B, plan.O[t]), dtype=dt, device=device)
+                if plan.T == 1:  # step f is the identity: the output gathers from Y
+                    self.buf[r]["recv_f"] = self.buf[r]["Y"].view(-1)
         self.asm_out = {}
         for r in self.local:
             b = self.buf[r]

@@ -70,7 +70,9 @@ class LoopbackFabric(Fabric):
                 soff = _offsets(send_splits[src])[j]
                 s, d = send[src], recv[dst]
                 es = s.element_size()
-                copies.append((s.data_ptr() + soff * es, d.data_ptr() + roffs[i] * es, cnt * es))
+                sp, dp = s.data_ptr() + soff * es, d.data_ptr() + roffs[i] * es
+                if sp != dp:  # aliased identity exchange (singleton group) moves nothing
+                    copies.append((sp, dp, cnt * es))
         K.CopyTable(copies, self.device).run()
 
     def exchange_counts(self, group, counts):
@@ -119,7 +121,7 @@ class NcclFabric(Fabric):
                 trace.record_elements(label, r, dst, int(send_splits[r][j]), elem_bytes)
         if len(group) == 1:
             n = int(send_splits[r][0])
-            if n:
+            if n and send[r].data_ptr() != recv[r].data_ptr():
                 recv[r][:n].copy_(send[r][:n])
             return
         self.dist.all_to_all_single(recv[r][: sum(recv_splits[r])], send[r][: sum(send_splits[r])],

@@ -129,17 +129,22 @@ class SpttEngine:
             b = {"send_x": torch.empty(max(1, nsend), dtype=dtype, device=dev),
                  "grad_x": torch.empty(max(1, nsend), dtype=dtype, device=dev)}
             if sptt:
-                b["recv_d"] = torch.empty(max(1, sum(p.d_recv_splits(r))), dtype=dtype, device=dev)
+                # singleton tower (W = 1): step d is the identity -> alias
+                b["recv_d"] = (b["send_x"] if p.W == 1 else
+                               torch.empty(max(1, sum(p.d_recv_splits(r))), dtype=dtype, device=dev))
                 b["X"] = torch.empty((p.T * p.B, p.x_width(r)), dtype=dtype, device=dev)
                 t = p.tower_of(r)
                 if t not in self.tm and p.O[t] == p.x_width(r):
                     b["Y"] = b["X"]  # pass-through tower: X is the step-f send buffer
                 else:
                     b["Y"] = torch.zeros((p.T * p.B, p.O[t]), dtype=dtype, device=dev)
-                b["recv_f"] = torch.empty(max(1, sum(p.f_recv_splits(r))), dtype=dtype, device=dev)
+                # singleton class (T = 1): step f is the identity -> alias
+                b["recv_f"] = (b["Y"].view(-1) if p.T == 1 else
+                               torch.empty(max(1, sum(p.f_recv_splits(r))), dtype=dtype, device=dev))
                 b["out"] = torch.empty((p.B, p.out_width()), dtype=dtype, device=dev)
             else:
-                b["recv_c"] = torch.empty(max(1, sum(p.c_recv_splits(r))), dtype=dtype, device=dev)
+                b["recv_c"] = (b["send_x"] if p.G == 1 else
+                               torch.empty(max(1, sum(p.c_recv_splits(r))), dtype=dtype, device=dev))
                 b["out"] = torch.empty((p.B, p.flat_width()), dtype=dtype, device=dev)
             self.buf[r] = b
             self.seg_fwd[r] = self._segments(r, b["send_x"])
@@ -223,6 +228,9 @@ class SpttEngine:
             recv_val_splits = fab.exchange_counts(world, val_splits)
         recv_len, recv_val = {}, {}
         for r in self.local:
+            if p.G == 1:  # single rank: step a is the identity
+                recv_len[r], recv_val[r] = send_len[r], send_val[r]
+                continue
             recv_len[r] = torch.empty(max(1, p.owner_bags(r)), dtype=torch.int32, device=dev)
             recv_val[r] = torch.empty(max(1, sum(recv_val_splits[r])), dtype=torch.int32, device=dev)
         with self._t("exchange"):
@@ -346,7 +354,8 @@ class SpttEngine:
                 off += p.B * p.O[t]
             K.Copy2DTable(copies, dev).run()
             gsend[r] = gf
-            grecv[r] = torch.empty((p.T * p.B, p.O[p.tower_of(r)]), dtype=self.dtype, device=dev)
+            grecv[r] = (gf.view(p.T * p.B, p.O[p.tower_of(r)]) if p.T == 1 else
+                        torch.empty((p.T * p.B, p.O[p.tower_of(r)]), dtype=self.dtype, device=dev))
         for g in self._groups(p.class_group_of):
             with self._t("exchange"):
                 fab.alltoallv(g, "f_bwd", gsend, {r: p.f_recv_splits(r) for r in g}, {r: grecv[r].view(-1) for r in self.local},
@@ -374,7 +383,7 @@ class SpttEngine:
         # d^-1: scatter dX columns back into the step-d receive layout
         dsend, drecv = {}, {}
         for r in self.local:
-            gd = torch.empty_like(self.buf[r]["recv_d"])
+            gd = self.buf[r]["grad_x"] if p.W == 1 else torch.empty_like(self.buf[r]["recv_d"])
             copies = []
             xw = p.x_width(r)
             for fb in p.e_blocks(r):
@@ -395,7 +404,7 @@ class SpttEngine:
         gsend = {}
         fw = p.flat_width()
         for r in self.local:
-            gc = torch.empty_like(self.buf[r]["recv_c"])
+            gc = self.buf[r]["grad_x"] if p.G == 1 else torch.empty_like(self.buf[r]["recv_c"])
             copies = []
             for fb in p.c_blocks():
                 for pc in fb.pieces:

@@ -279,28 +279,36 @@ class TowerModule:
         return dx
 
     def _dcn_bwd(self, gy):
+        """Crossnet backward with the element-wise work fused into GEMM
+        epilogues (dmt_gemm DCN_BWD / DCN_FINAL):
+            g_L = gy Wp;  gu_l = g_{l+1} * x0;  dx0 += g_{l+1} * u_l
+            dW_l = gu_l^T x_l;  g_l = gu_l W_l + g_{l+1};  dX = g_0 + dx0
+        (derivative of towermod.py:132-158; x_0 = X, u_l = x_l W_l^T + b_l)."""
         xs, us = self._saved
         x0 = xs[0]
         rows, M = x0.shape
+        L_ = self.cfg.cross_layers
         f32 = torch.float32
-        self.grads["w_proj"] = K.gemm(gy, xs[-1], torch.empty(self.w["w_proj"].shape, dtype=f32, device=x0.device),
+        dev = x0.device
+        self.grads["w_proj"] = K.gemm(gy, xs[-1], torch.empty(self.w["w_proj"].shape, dtype=f32, device=dev),
                                       trans_a=True, trans_b=True)
         self.grads["b_proj"] = K.column_sum(gy)
-        g = torch.empty((rows, M), dtype=self.dtype, device=x0.device)
-        K.gemm(gy, self.w["w_proj"], g, trans_b=True)
-        dx0 = torch.zeros((rows, M), dtype=f32, device=x0.device)
-        gu = torch.empty_like(g)
-        for layer in range(self.cfg.cross_layers - 1, -1, -1):
-            K.cross_bwd_pointwise(g, x0, us[layer], gu, dx0)
-            self.grads[f"w{layer}"] = K.gemm(gu, xs[layer], torch.empty((M, M), dtype=f32, device=x0.device),
-                                             trans_a=True, trans_b=True)
-            self.grads[f"b{layer}"] = K.column_sum(gu)
-            # g <- gu @ W + g   (in-place accumulate epilogue)
-            K.gemm(gu, self.w[f"w{layer}"], g, epilogue=L.EPI_ACC, beta=1.0, trans_b=True)
-        # dX = dx0 + g
+        g = torch.empty((rows, M), dtype=self.dtype, device=dev)
+        gu = [torch.empty((rows, M), dtype=self.dtype, device=dev) for _ in range(2)]
+        dx0 = torch.empty((rows, M), dtype=f32, device=dev)
+        K.gemm(gy, self.w["w_proj"], g, trans_b=True, epilogue=L.EPI_DCN_BWD, x0=x0, xl=us[L_ - 1],
+               aux=gu[(L_ - 1) % 2], aux2=dx0, aux2_accum=False)
         dx = torch.empty_like(g)
-        tmp = K.convert(dx0, self.dtype)
-        K.assemble([K.Block(0, M, [(g, 0, M), (tmp, 0, M)])], dx, rows)
+        for layer in range(L_ - 1, -1, -1):
+            cur = gu[layer % 2]
+            self.grads[f"w{layer}"] = K.gemm(cur, xs[layer], torch.empty((M, M), dtype=f32, device=dev),
+                                             trans_a=True, trans_b=True)
+            self.grads[f"b{layer}"] = K.column_sum(cur)
+            if layer > 0:
+                K.gemm(cur, self.w[f"w{layer}"], g, trans_b=True, epilogue=L.EPI_DCN_BWD, c=g, beta=1.0, x0=x0,
+                       xl=us[layer - 1], aux=gu[(layer - 1) % 2], aux2=dx0, aux2_accum=True)
+            else:
+                K.gemm(cur, self.w["w0"], dx, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=g, beta=1.0, aux2=dx0)
         return dx
 
     def sgd_step(self, lr: float) -> None:
