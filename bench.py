@@ -256,43 +256,77 @@ def main():
         if world > 1:
             dist.barrier(device_ids=[local])
 
-    def timed(m, K, Wm, host_inputs=None):
+    def timed_eager(m, K, Wm):
+        """Eager steps with per-phase CUDA events (phase breakdown + fallback)."""
         for i in range(Wm):
             m.train_step(batches[i % len(batches)], gout)
         torch.cuda.synchronize()
         barrier()
-        torch.cuda.synchronize()
         timers = PhaseTimers()
         m.engine.timers = timers
         calls0 = _lib.CALLS[0]
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         for i in range(K):
-            if host_inputs is None:
-                m.train_step(batches[i % len(batches)], gout)
-            else:
-                hl, hv, nnz = host_inputs[i % len(host_inputs)]
-                kj = KJT(hl.to(dev, non_blocking=True), hv.to(dev, non_blocking=True), nnz, B)
-                outs = m.train_step({rank: kj}, gout)
-                loss = torch.dot(outs[rank].view(-1).float(), gout[rank].view(-1).float())
-                loss.cpu()
+            m.train_step(batches[i % len(batches)], gout)
         e.record()
         torch.cuda.synchronize()
         barrier()
         m.engine.timers = None
-        ms = s.elapsed_time(e)
+        return s.elapsed_time(e), timers, (_lib.CALLS[0] - calls0) // max(K, 1)
+
+    def max_over_ranks(ms):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item()), timers, _lib.CALLS[0] - calls0
+        return float(t.item())
 
+    def timed_graph(m, K, host_inputs=None):
+        """The timed region: K CUDA-graph replays of the whole train step.  Each
+        step first copies its batch into the graph's static input buffers
+        (device->device, or pinned host->device for e2e) inside the region."""
+        st = {rank: KJT(batches[0][rank].lengths.clone(), batches[0][rank].values.clone(),
+                        batches[0][rank].nnz_per_feature, B)}
+        replay, outs = m.capture(st, gout)
+        loss_dev = torch.zeros((), dtype=torch.float32, device=dev)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for i in range(K):
+            if host_inputs is None:
+                src = batches[i % len(batches)][rank]
+                st[rank].lengths.copy_(src.lengths, non_blocking=True)
+                st[rank].values.copy_(src.values, non_blocking=True)
+                replay()
+            else:
+                hl, hv, _ = host_inputs[i % len(host_inputs)]
+                st[rank].lengths.copy_(hl, non_blocking=True)
+                st[rank].values.copy_(hv, non_blocking=True)
+                replay()
+                torch.dot(outs[rank].view(-1).float(), gout[rank].view(-1).float(), out=loss_dev)
+                loss_dev.cpu()
+        e.record()
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(s.elapsed_time(e))
+
+    # per-phase breakdown (eager, instrumented) -- also the fallback timing
+    eager_ms, timers, calls = timed_eager(model, args.steps, args.warmup)
+    ph = {k: v / args.steps for k, v in timers.ms().items()}
+    graph_ok = True
     clocks = ClockSampler(local)
     clocks.start()
-    total_ms, timers, calls = timed(model, args.steps, args.warmup)
+    try:
+        total_ms = timed_graph(model, args.steps)
+    except Exception as ex:  # capture unsupported (e.g. collective backend): eager numbers
+        graph_ok = False
+        graph_err = repr(ex)[:200]
+        total_ms = max_over_ranks(eager_ms)
     clk = clocks.stop()
     ms_step = total_ms / args.steps
     value = N * B * args.steps / (total_ms / 1000.0)
-    ph = {k: v / args.steps for k, v in timers.ms().items()}
 
     # e2e through the public API with host (pinned) inputs
     e2e = None
@@ -301,7 +335,10 @@ def main():
         for bt in batches:
             kj = bt[rank]
             hosts.append((kj.lengths.cpu().pin_memory(), kj.values.cpu().pin_memory(), kj.nnz_per_feature))
-        e_ms, _, _ = timed(model, args.steps, 2, host_inputs=hosts)
+        if graph_ok:
+            e_ms = timed_graph(model, args.steps, host_inputs=hosts)
+        else:
+            e_ms = max_over_ranks(eager_ms)
         h2d = hosts[0][0].numel() * 4 + hosts[0][1].numel() * 4
         e2e = {"value": N * B * args.steps / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 4}
@@ -346,9 +383,11 @@ def main():
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic (uniform random rows, random-init tables and TM weights)",
         "config": _config(args, N), "roofline": roof, "roofline_lookup": roof_lookup,
-        "lookup_hbm_gbs": look_gbs, "phases_ms_per_step": ph,
+        "lookup_hbm_gbs": look_gbs, "phases_ms_per_step": ph, "cuda_graph": graph_ok,
+        "eager_ms_per_step": max_over_ranks(eager_ms) / args.steps,
         "exposed_comm_ms_per_step": ph.get("exchange", 0.0), "clocks": clk, "e2e": e2e,
-        "gpu_launches": calls, "gpu_launches_note": "libdmt entry-point calls in the timed region (each >= 1 kernel)",
+        "gpu_launches": calls * args.steps,
+        "gpu_launches_note": "libdmt entry-point calls per step x steps (each >= 1 kernel; replayed from a CUDA graph)",
     }
     # flat all-to-all baseline alongside (N > 1)
     if N > 1 and not args.no_flat:
@@ -357,12 +396,18 @@ def main():
         flat = SPTT(topo, layout, placement, assignment, pooling, B, fabric, tm=tm_cfg, dtype=dtype, device=dev,
                     mode="flat", lr=1e-3)
         gout = {rank: (torch.randn(B, flat.out_width, generator=gen, device=dev) * 1e-3).to(dtype)}
-        f_ms, f_t, _ = timed(flat, args.steps, args.warmup)
+        fe_ms, f_t, _ = timed_eager(flat, args.steps, args.warmup)
         fph = {k: v / args.steps for k, v in f_t.ms().items()}
+        try:
+            f_ms = timed_graph(flat, args.steps) if graph_ok else max_over_ranks(fe_ms)
+        except Exception:
+            f_ms = max_over_ranks(fe_ms)
         result["flat_baseline"] = {"value": N * B * args.steps / (f_ms / 1000.0), "ms_per_step": f_ms / args.steps,
                                    "exposed_comm_ms_per_step": fph.get("exchange", 0.0), "phases_ms_per_step": fph}
     if rank == 0 and N == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(args)
+    if not graph_ok:
+        result["cuda_graph_error"] = graph_err
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:

@@ -24,15 +24,61 @@ def _dt(t: torch.Tensor) -> int:
         raise DomainError(f"unsupported dtype {t.dtype}") from None
 
 
+_TABLE_CACHE: dict = {}
+
+
 def device_table(ctype, items: Sequence, device) -> tuple[torch.Tensor, object]:
-    """Upload a list of ctypes structs; returns (device bytes, host array)."""
+    """Upload a list of ctypes structs; returns (device bytes, host array).
+
+    Content-addressed: an identical table (same descriptors, same buffer
+    pointers) is uploaded once and reused, so steady-state steps issue no
+    host->device descriptor copies -- which is what makes a whole training
+    step capturable as one CUDA graph."""
     arr = (ctype * max(1, len(items)))()
     for i, it in enumerate(items):
         arr[i] = it
     nbytes = C.sizeof(ctype) * max(1, len(items))
-    buf = bytearray(C.string_at(C.addressof(arr), nbytes))
-    dev = torch.frombuffer(buf, dtype=torch.uint8).to(device)
+    raw = C.string_at(C.addressof(arr), nbytes)
+    key = (ctype.__name__, str(device), raw)
+    dev = _TABLE_CACHE.get(key)
+    if dev is None:
+        dev = _upload(raw, device)
+        if len(_TABLE_CACHE) > 4096 and not torch.cuda.is_current_stream_capturing():
+            _TABLE_CACHE.clear()
+        _TABLE_CACHE[key] = dev
     return dev, arr
+
+
+_PINNED_KEEPALIVE: list = []
+
+
+def _upload(raw: bytes, device) -> torch.Tensor:
+    """Bytes -> device.  Inside CUDA-graph capture the copy is recorded from a
+    pinned host buffer that is kept alive (its content never changes, so every
+    replay re-installs the same descriptors)."""
+    if torch.cuda.is_current_stream_capturing():
+        host = torch.frombuffer(bytearray(raw), dtype=torch.uint8).pin_memory()
+        _PINNED_KEEPALIVE.append(host)
+        dev = torch.empty(len(raw), dtype=torch.uint8, device=device)
+        dev.copy_(host, non_blocking=True)
+        return dev
+    return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)
+
+
+_INT_CACHE: dict = {}
+
+
+def device_ints(values: Sequence[int], dtype: torch.dtype, device) -> torch.Tensor:
+    """Content-addressed small integer array on the device (e.g. slot offsets)."""
+    key = (tuple(int(v) for v in values), dtype, str(device))
+    t = _INT_CACHE.get(key)
+    if t is None:
+        host = torch.tensor(key[0] or (0,), dtype=dtype)
+        t = _upload(host.numpy().tobytes(), device).view(dtype)
+        if len(_INT_CACHE) > 4096 and not torch.cuda.is_current_stream_capturing():
+            _INT_CACHE.clear()
+        _INT_CACHE[key] = t
+    return t
 
 
 # ------------------------------------------------------------------ KJT ----

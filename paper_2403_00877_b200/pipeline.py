@@ -157,9 +157,19 @@ class SpttEngine:
                 self.asm_c[r] = self._assemble_table(p.c_blocks(), b["recv_c"], b["out"], p.B)
         self._bwd_ws = {}
         self.timers: Optional[PhaseTimers] = None
+        self.uniform_nnz = False
 
     def _t(self, name: str):
         return _Scope(self.timers, name)
+
+    def _persist(self, r: int, name: str, like: torch.Tensor) -> torch.Tensor:
+        """Backward scratch kept across steps (stable pointers -> cached
+        descriptor tables, capturable)."""
+        t = self.buf[r].get(name)
+        if t is None:
+            t = torch.empty_like(like)
+            self.buf[r][name] = t
+        return t
 
     # ----------------------------------------------------------- tables ----
     def _segments(self, r: int, out: torch.Tensor, with_keys: bool = False) -> K.SegmentTable:
@@ -214,18 +224,25 @@ class SpttEngine:
             kj = kjts[r]
             if kj.B != p.B or kj.F != len(p.features):
                 raise DomainError("KJT shape does not match the plan")
-            offs = kj.ensure_offsets()
+            offs = kj.offsets if kj.offsets is not None else K.lengths_to_offsets(kj.lengths)
             slot_offs = p.a_slot_value_offsets(kj.nnz_per_feature)
             total = slot_offs[-1]
             send_len[r] = torch.empty(max(1, len(p.a_slots) * p.B), dtype=torch.int32, device=dev)
             send_val[r] = torch.empty(max(1, total), dtype=torch.int32, device=dev)
             if p.a_slots:
-                so = torch.tensor(slot_offs, dtype=torch.int64).to(dev, non_blocking=True)
+                so = K.device_ints(slot_offs, torch.int64, dev)
                 K.kjt_bucketize(kj.lengths, offs, kj.values, p.B, self.slot_feature, so, send_len[r], send_val[r])
             len_splits[r] = p.a_send_length_splits()
             val_splits[r] = p.a_send_value_splits(kj.nnz_per_feature)
-        with self._t("exchange"):
-            recv_val_splits = fab.exchange_counts(world, val_splits)
+        if self.uniform_nnz:
+            # fixed pooling factors: every rank ships the same per-feature nnz,
+            # so owner r receives val_splits[r][r] from every source and the
+            # ragged step-a splits need no counts exchange (no host sync -> the
+            # step is CUDA-graph capturable)
+            recv_val_splits = {r: [val_splits[r][r]] * p.G for r in self.local}
+        else:
+            with self._t("exchange"):
+                recv_val_splits = fab.exchange_counts(world, val_splits)
         recv_len, recv_val = {}, {}
         for r in self.local:
             if p.G == 1:  # single rank: step a is the identity
@@ -344,7 +361,7 @@ class SpttEngine:
         # receive layout), send each block back to the member that produced it
         gsend, grecv = {}, {}
         for r in self.local:
-            gf = torch.empty_like(self.buf[r]["recv_f"])
+            gf = self._persist(r, "g_f", self.buf[r]["recv_f"])
             copies = []
             col, off = 0, 0
             ow = p.out_width()
@@ -355,7 +372,7 @@ class SpttEngine:
             K.Copy2DTable(copies, dev).run()
             gsend[r] = gf
             grecv[r] = (gf.view(p.T * p.B, p.O[p.tower_of(r)]) if p.T == 1 else
-                        torch.empty((p.T * p.B, p.O[p.tower_of(r)]), dtype=self.dtype, device=dev))
+                        self._persist(r, "g_y", self.buf[r]["Y"]))
         for g in self._groups(p.class_group_of):
             with self._t("exchange"):
                 fab.alltoallv(g, "f_bwd", gsend, {r: p.f_recv_splits(r) for r in g}, {r: grecv[r].view(-1) for r in self.local},
@@ -383,7 +400,7 @@ class SpttEngine:
         # d^-1: scatter dX columns back into the step-d receive layout
         dsend, drecv = {}, {}
         for r in self.local:
-            gd = self.buf[r]["grad_x"] if p.W == 1 else torch.empty_like(self.buf[r]["recv_d"])
+            gd = self.buf[r]["grad_x"] if p.W == 1 else self._persist(r, "g_d", self.buf[r]["recv_d"])
             copies = []
             xw = p.x_width(r)
             for fb in p.e_blocks(r):
@@ -404,7 +421,7 @@ class SpttEngine:
         gsend = {}
         fw = p.flat_width()
         for r in self.local:
-            gc = self.buf[r]["grad_x"] if p.G == 1 else torch.empty_like(self.buf[r]["recv_c"])
+            gc = self.buf[r]["grad_x"] if p.G == 1 else self._persist(r, "g_c", self.buf[r]["recv_c"])
             copies = []
             for fb in p.c_blocks():
                 for pc in fb.pieces:

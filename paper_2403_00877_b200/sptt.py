@@ -109,6 +109,29 @@ class SPTT:
         self.backward(grads)
         return outs
 
+    def capture(self, kjts: dict, grads: dict, warmup: int = 2):
+        """Capture one full train step (forward a-f, backward, optimizer
+        updates) as a CUDA graph over the given static input buffers.
+
+        Returns (replay, outs): copy the next batch into ``kjts``' lengths /
+        values in place, then call replay().  Requires fixed per-feature nnz
+        (uniform_nnz: no step-a counts exchange / host sync) and a fixed batch
+        shape.  Every launch inside is a libdmt kernel or an NCCL collective on
+        the capture stream; descriptor tables are content-cached, so replay
+        issues no host work besides the graph launch."""
+        self.engine.uniform_nnz = True
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.train_step(kjts, grads)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            outs = self.train_step(kjts, grads)
+        return graph.replay, outs
+
 
 def build_world(G_hosts: int, ranks_per_host: int, hosts_per_tower: int, num_tables: int, rows: int, dim: int,
                 seed: int = 0, dtype=np.float32, scheme: str = "table_wise", shards_per_table: int = 1,
