@@ -288,25 +288,50 @@ def main():
         st = {rank: KJT(batches[0][rank].lengths.clone(), batches[0][rank].values.clone(),
                         batches[0][rank].nnz_per_feature, B)}
         replay, outs = m.capture(st, gout)
-        loss_dev = torch.zeros((), dtype=torch.float32, device=dev)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        for i in range(K):
-            if host_inputs is None:
+        if host_inputs is None:
+            for i in range(K):
                 src = batches[i % len(batches)][rank]
                 st[rank].lengths.copy_(src.lengths, non_blocking=True)
                 st[rank].values.copy_(src.values, non_blocking=True)
                 replay()
-            else:
-                hl, hv, _ = host_inputs[i % len(host_inputs)]
-                st[rank].lengths.copy_(hl, non_blocking=True)
-                st[rank].values.copy_(hv, non_blocking=True)
+        else:
+            # e2e input pipeline: the pinned host batch of step i+1 is copied to
+            # a device staging buffer on a copy stream while step i runs; each
+            # step's loss is read back to pinned host memory asynchronously.
+            cs = torch.cuda.Stream()
+            stage = [(torch.empty_like(st[rank].lengths), torch.empty_like(st[rank].values)) for _ in range(2)]
+            ready = [torch.cuda.Event() for _ in range(2)]
+            free = [torch.cuda.Event() for _ in range(2)]
+            losses = torch.zeros(K, dtype=torch.float32).pin_memory()
+            loss_buf = torch.zeros(K, dtype=torch.float32, device=dev)
+
+            def prefetch(j):
+                hl, hv, _ = host_inputs[j % len(host_inputs)]
+                with torch.cuda.stream(cs):
+                    cs.wait_event(free[j % 2])
+                    stage[j % 2][0].copy_(hl, non_blocking=True)
+                    stage[j % 2][1].copy_(hv, non_blocking=True)
+                    ready[j % 2].record(cs)
+
+            for ev in free:
+                ev.record()
+            prefetch(0)
+            for i in range(K):
+                cur = i % 2
+                torch.cuda.current_stream().wait_event(ready[cur])
+                st[rank].lengths.copy_(stage[cur][0], non_blocking=True)
+                st[rank].values.copy_(stage[cur][1], non_blocking=True)
+                free[cur].record()
+                if i + 1 < K:
+                    prefetch(i + 1)
                 replay()
-                torch.dot(outs[rank].view(-1).float(), gout[rank].view(-1).float(), out=loss_dev)
-                loss_dev.cpu()
+                torch.dot(outs[rank].view(-1).float(), gout[rank].view(-1).float(), out=loss_buf[i])
+                losses[i:i + 1].copy_(loss_buf[i:i + 1], non_blocking=True)
         e.record()
         torch.cuda.synchronize()
         barrier()

@@ -127,6 +127,19 @@ int dmt_pooled_lookup_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segme
                           float lr, float eps, void* workspace, size_t workspace_bytes,
                           dmt_stream_t stream);
 
+/* The same in two halves: _prepare (sort keys, per-bag records, radix sort)
+ * needs only the indices and can run while the tower module computes; _apply
+ * (segment reduce + optimizer) then consumes the gradients.  Both must use the
+ * same workspace, segment table and sizes. */
+int dmt_pooled_lookup_bwd_prepare(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host,
+                                  int32_t num_segs, const int64_t* offsets, const int32_t* indices,
+                                  int64_t nnz, int64_t key_space, int32_t dtype, void* workspace,
+                                  size_t workspace_bytes, dmt_stream_t stream);
+int dmt_pooled_lookup_bwd_apply(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host,
+                                int32_t num_segs, int64_t nnz, int64_t key_space, int32_t dtype,
+                                int32_t optimizer, float lr, float eps, void* workspace,
+                                size_t workspace_bytes, dmt_stream_t stream);
+
 /* ------------------------------------------------------------ assemble ---- */
 
 /* dst[r, col0 + j] = sum_{s < nsrc} src_s[r*ld_s + j]   for r < rows, j < width.

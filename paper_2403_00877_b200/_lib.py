@@ -73,6 +73,8 @@ _SIGS = {
     "dmt_pooled_lookup_fwd": (C.c_int, [vp, vp, i32, vp, vp, i32, vp, vp]),
     "dmt_pooled_lookup_bwd_workspace_size": (sz, [i64, i64, i64]),
     "dmt_pooled_lookup_bwd": (C.c_int, [vp, vp, i32, vp, vp, i64, i64, i32, i32, f32, f32, vp, sz, vp]),
+    "dmt_pooled_lookup_bwd_prepare": (C.c_int, [vp, vp, i32, vp, vp, i64, i64, i32, vp, sz, vp]),
+    "dmt_pooled_lookup_bwd_apply": (C.c_int, [vp, vp, i32, i64, i64, i32, i32, f32, f32, vp, sz, vp]),
     "dmt_assemble": (C.c_int, [vp, i32, i32, vp, i64, vp, i64, i32, vp]),
     "dmt_batched_copy": (C.c_int, [vp, i32, i64, vp]),
     "dmt_batched_copy2d": (C.c_int, [vp, i32, i32, i64, vp]),

@@ -436,7 +436,9 @@ inline BwdLayout bwd_layout(int64_t nnz, int64_t key_space, int64_t nbags) {
 template <typename T>
 int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int32_t n, const int64_t* offsets,
                const int32_t* indices, int64_t nnz, int64_t key_space, int32_t opt, float lr, float eps,
-               void* ws, size_t ws_bytes, cudaStream_t s) {
+               void* ws, size_t ws_bytes, cudaStream_t s, int phase) {
+  // phase bit 1: keys + bag records + radix sort (needs only the indices);
+  // phase bit 2: the fused reduce + optimizer update (needs the gradients)
   if (nnz <= 0 || n == 0) return DMT_OK;
   if ((uint64_t)key_space >= 0xFFFFFFFFull || nnz > 0x7FFFFFFF) return DMT_ERR_UNSUPPORTED;
   int max_b = 0, max_w = 0;
@@ -461,13 +463,16 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
   BagRec* recs = (BagRec*)(w + L.recs);
   const uint32_t invalid = (uint32_t)key_space;
 
-  dim3 kg((unsigned)ceil_div((int64_t)max_b * 8, 256), n);
-  bwd_keys_kernel<<<kg, 256, 0, s>>>(segs, offsets, indices, invalid, keys_in, vals_in, recs, (int)sizeof(T));
-  DMT_CHECK_LAUNCH();
-  size_t cub_bytes = L.cub_bytes;
-  if (cub::DeviceRadixSort::SortPairs((void*)(w + L.cub_temp), cub_bytes, keys_in, keys_out, vals_in, vals_out,
-                                      (int)nnz, 0, end_bit_for((uint64_t)key_space), s) != cudaSuccess)
-    return DMT_ERR_CUDA;
+  if (phase & 1) {
+    dim3 kg((unsigned)ceil_div((int64_t)max_b * 8, 256), n);
+    bwd_keys_kernel<<<kg, 256, 0, s>>>(segs, offsets, indices, invalid, keys_in, vals_in, recs, (int)sizeof(T));
+    DMT_CHECK_LAUNCH();
+    size_t cub_bytes = L.cub_bytes;
+    if (cub::DeviceRadixSort::SortPairs((void*)(w + L.cub_temp), cub_bytes, keys_in, keys_out, vals_in, vals_out,
+                                        (int)nnz, 0, end_bit_for((uint64_t)key_space), s) != cudaSuccess)
+      return DMT_ERR_CUDA;
+  }
+  if (!(phase & 2)) return DMT_OK;
   constexpr int VEC = Vec16<T>::N;
   bool vec_ok = true;
   for (int i = 0; i < n; ++i) {
@@ -537,24 +542,47 @@ size_t dmt_pooled_lookup_bwd_workspace_size(int64_t nnz, int64_t key_space, int6
   return dmt::bwd_layout(nnz, key_space, num_bags).total;
 }
 
-int dmt_pooled_lookup_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host, int32_t num_segs,
-                          const int64_t* offsets, const int32_t* indices, int64_t nnz, int64_t key_space,
-                          int32_t dtype, int32_t optimizer, float lr, float eps, void* workspace,
-                          size_t workspace_bytes, dmt_stream_t stream) {
+static int bwd_dispatch(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host, int32_t num_segs,
+                        const int64_t* offsets, const int32_t* indices, int64_t nnz, int64_t key_space,
+                        int32_t dtype, int32_t optimizer, float lr, float eps, void* workspace,
+                        size_t workspace_bytes, dmt_stream_t stream, int phase) {
   if (num_segs < 0 || nnz < 0) return DMT_ERR_DOMAIN;
   cudaStream_t s = (cudaStream_t)stream;
   switch (dtype) {
     case DMT_F32:
       return dmt::launch_bwd<float>(segs, segs_host, num_segs, offsets, indices, nnz, key_space, optimizer, lr,
-                                    eps, workspace, workspace_bytes, s);
+                                    eps, workspace, workspace_bytes, s, phase);
     case DMT_BF16:
       return dmt::launch_bwd<__nv_bfloat16>(segs, segs_host, num_segs, offsets, indices, nnz, key_space,
-                                            optimizer, lr, eps, workspace, workspace_bytes, s);
+                                            optimizer, lr, eps, workspace, workspace_bytes, s, phase);
     case DMT_F64:
       return dmt::launch_bwd<double>(segs, segs_host, num_segs, offsets, indices, nnz, key_space, optimizer, lr,
-                                     eps, workspace, workspace_bytes, s);
+                                     eps, workspace, workspace_bytes, s, phase);
     default: return DMT_ERR_UNSUPPORTED;
   }
+}
+
+int dmt_pooled_lookup_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host, int32_t num_segs,
+                          const int64_t* offsets, const int32_t* indices, int64_t nnz, int64_t key_space,
+                          int32_t dtype, int32_t optimizer, float lr, float eps, void* workspace,
+                          size_t workspace_bytes, dmt_stream_t stream) {
+  return bwd_dispatch(segs, segs_host, num_segs, offsets, indices, nnz, key_space, dtype, optimizer, lr, eps,
+                      workspace, workspace_bytes, stream, 3);
+}
+
+int dmt_pooled_lookup_bwd_prepare(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host,
+                                  int32_t num_segs, const int64_t* offsets, const int32_t* indices, int64_t nnz,
+                                  int64_t key_space, int32_t dtype, void* workspace, size_t workspace_bytes,
+                                  dmt_stream_t stream) {
+  return bwd_dispatch(segs, segs_host, num_segs, offsets, indices, nnz, key_space, dtype, DMT_OPT_SGD, 0.f, 0.f,
+                      workspace, workspace_bytes, stream, 1);
+}
+
+int dmt_pooled_lookup_bwd_apply(const dmt_lookup_segment* segs, const dmt_lookup_segment* segs_host,
+                                int32_t num_segs, int64_t nnz, int64_t key_space, int32_t dtype, int32_t optimizer,
+                                float lr, float eps, void* workspace, size_t workspace_bytes, dmt_stream_t stream) {
+  return bwd_dispatch(segs, segs_host, num_segs, nullptr, nullptr, nnz, key_space, dtype, optimizer, lr, eps,
+                      workspace, workspace_bytes, stream, 2);
 }
 
 }  // extern "C"

@@ -191,6 +191,26 @@ def pooled_lookup_bwd(table: SegmentTable, offsets, indices, nnz: int, key_space
             "dmt_pooled_lookup_bwd")
 
 
+def pooled_lookup_bwd_prepare(table: SegmentTable, offsets, indices, nnz: int, key_space: int,
+                              workspace: torch.Tensor) -> None:
+    if table.n == 0 or nnz == 0:
+        return
+    L.check(L.lib().dmt_pooled_lookup_bwd_prepare(table.dev.data_ptr(), C.addressof(table.host), table.n,
+                                                  offsets.data_ptr(), indices.data_ptr(), nnz, key_space,
+                                                  L.TORCH_DT[table.dtype], workspace.data_ptr(), workspace.numel(),
+                                                  L.stream_ptr()), "dmt_pooled_lookup_bwd_prepare")
+
+
+def pooled_lookup_bwd_apply(table: SegmentTable, nnz: int, key_space: int, optimizer: int, lr: float, eps: float,
+                            workspace: torch.Tensor) -> None:
+    if table.n == 0 or nnz == 0:
+        return
+    L.check(L.lib().dmt_pooled_lookup_bwd_apply(table.dev.data_ptr(), C.addressof(table.host), table.n, nnz,
+                                                key_space, L.TORCH_DT[table.dtype], optimizer, lr, eps,
+                                                workspace.data_ptr(), workspace.numel(), L.stream_ptr()),
+            "dmt_pooled_lookup_bwd_apply")
+
+
 # ------------------------------------------------------------ assemble ----
 @dataclass
 class Block:

@@ -158,6 +158,8 @@ class SpttEngine:
         self._bwd_ws = {}
         self.timers: Optional[PhaseTimers] = None
         self.uniform_nnz = False
+        self._side = None
+        self._prepared: dict = {}
 
     def _t(self, name: str):
         return _Scope(self.timers, name)
@@ -262,7 +264,18 @@ class SpttEngine:
             offsets = K.lengths_to_offsets(recv_len[r][: p.owner_bags(r)])
             with self._t("lookup_fwd"):
                 K.pooled_lookup_fwd(self.seg_fwd[r], offsets, recv_val[r], err)
-            self._owner[r] = (offsets, recv_val[r], sum(recv_val_splits[r]))
+            nnz = sum(recv_val_splits[r])
+            self._owner[r] = (offsets, recv_val[r], nnz)
+            if save:
+                # the embedding backward's key build + radix sort need only the
+                # indices: run them on a side stream, overlapped with the tower
+                # module forward/backward and the exchanges (joined in backward)
+                side = self._side_stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    K.pooled_lookup_bwd_prepare(self.seg_bwd[r], offsets, recv_val[r], nnz, self.key_space[r],
+                                                self._bwd_workspace(r, nnz))
+                self._prepared[r] = True
         if err is not None:
             K.raise_lookup_errors(err)
         if self.mode == "flat":
@@ -433,16 +446,31 @@ class SpttEngine:
                           {r: self.buf[r]["grad_x"] for r in self.local}, {r: p.c_send_splits(r) for r in world})
         self._embedding_update(lr, optimizer, eps)
 
+    def _side_stream(self):
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        return self._side
+
+    def _bwd_workspace(self, r: int, nnz: int) -> torch.Tensor:
+        need = L.lib().dmt_pooled_lookup_bwd_workspace_size(nnz, self.key_space[r], self.plan.owner_bags(r))
+        ws = self._bwd_ws.get(r)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(max(1, need), dtype=torch.uint8, device=self.device)
+            self._bwd_ws[r] = ws
+        return ws
+
     def _embedding_update(self, lr, optimizer, eps):
         if optimizer == L.OPT_ROWWISE_ADAGRAD and not self.state:
             self.enable_adagrad()
+            self._prepared = {}  # records must point at the new state arrays
         for r in self.local:
             offsets, vals, nnz = self._owner[r]
             ks = self.key_space[r]
-            need = L.lib().dmt_pooled_lookup_bwd_workspace_size(nnz, ks, self.plan.owner_bags(r))
-            ws = self._bwd_ws.get(r)
-            if ws is None or ws.numel() < need:
-                ws = torch.empty(max(1, need), dtype=torch.uint8, device=self.device)
-                self._bwd_ws[r] = ws
+            ws = self._bwd_workspace(r, nnz)
             with self._t("lookup_bwd"):
-                K.pooled_lookup_bwd(self.seg_bwd[r], offsets, vals, nnz, ks, optimizer, lr, eps, ws)
+                if self._prepared.get(r):
+                    torch.cuda.current_stream().wait_stream(self._side)
+                    K.pooled_lookup_bwd_apply(self.seg_bwd[r], nnz, ks, optimizer, lr, eps, ws)
+                else:
+                    K.pooled_lookup_bwd(self.seg_bwd[r], offsets, vals, nnz, ks, optimizer, lr, eps, ws)
+            self._prepared[r] = False
