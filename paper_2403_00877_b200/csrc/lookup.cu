@@ -400,6 +400,173 @@ bwd_update_kernel(const uint32_t* __restrict__ skeys, const int32_t* __restrict_
   }
 }
 
+// ---- fast path: no mean pooling, all gradient rows in one buffer ----------
+// The sort value is the gradient row's 16-byte offset from that buffer, and
+// the owning shard of a key is found in a small shard table copied to shared
+// memory, so a run head needs exactly two dependent levels of loads (sorted
+// key/value -> gradient row + weight row) instead of three.
+constexpr int kMaxShards = 96;
+struct ShardTab {
+  int n;
+  uint32_t key_base[kMaxShards];
+  uint16_t ld[kMaxShards];
+  uint16_t width[kMaxShards];
+  const char* weights[kMaxShards];
+  float* state[kMaxShards];
+};
+
+__global__ void bwd_keys_fast_kernel(const dmt_lookup_segment* __restrict__ segs,
+                                     const int64_t* __restrict__ offsets, const int32_t* __restrict__ indices,
+                                     uint32_t invalid, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                                     const char* __restrict__ gbase, int es) {
+  const dmt_lookup_segment& sg = segs[blockIdx.y];
+  const int sub = threadIdx.x & 7;
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  if (b >= sg.nbags) return;
+  const int64_t gb = sg.bag_begin + b;
+  const int64_t beg = offsets[gb], end = offsets[gb + 1];
+  const int32_t goff = (int32_t)((reinterpret_cast<const char*>(sg.out) + (size_t)(b * sg.out_ld) * es - gbase) >> 4);
+  for (int64_t k = beg + sub; k < end; k += 8) {
+    int64_t r = (int64_t)__ldg(indices + k) - sg.row_begin;
+    bool in = r >= 0 && r < sg.rows;
+    keys[k] = in ? (uint32_t)(sg.key_base + r) : invalid;
+    vals[k] = goff;
+  }
+}
+
+template <typename T, int VEC, int NV, int CH>
+__global__ void __launch_bounds__(kLookupThreads, 2)
+bwd_update_fast_kernel(const uint32_t* __restrict__ skeys, const int32_t* __restrict__ svals, int64_t nnz,
+                       const char* __restrict__ gbase, const __grid_constant__ ShardTab tab, uint32_t invalid,
+                       int log2g, int opt, float lr, float eps) {
+  using A = typename Acc<T>::type;
+  __shared__ uint32_t s_kb[kMaxShards];
+  __shared__ uint16_t s_ld[kMaxShards], s_w[kMaxShards];
+  __shared__ const char* s_wp[kMaxShards];
+  __shared__ float* s_st[kMaxShards];
+  for (int i = threadIdx.x; i < tab.n; i += blockDim.x) {
+    s_kb[i] = tab.key_base[i];
+    s_ld[i] = tab.ld[i];
+    s_w[i] = tab.width[i];
+    s_wp[i] = tab.weights[i];
+    s_st[i] = tab.state[i];
+  }
+  __syncthreads();
+  const int nsh = tab.n;
+  const int G = 1 << log2g;
+  const int t = threadIdx.x & (G - 1);
+  const int gpw = 32 >> log2g;
+  const int gin = (threadIdx.x & 31) >> log2g;
+  const int64_t warp_global = (int64_t)blockIdx.x * (kLookupThreads / 32) + (threadIdx.x >> 5);
+  const int64_t stride = (int64_t)gridDim.x * (kLookupThreads / 32) * gpw * CH;
+  // software pipeline: the sorted keys / values of the next chunk are loaded
+  // while the current chunk's rows are in flight
+  uint32_t nk[CH + 2];
+  int32_t ngv[CH];
+  auto fetch = [&](int64_t c0) {
+#pragma unroll
+    for (int u = 0; u <= CH; ++u) nk[u + 1] = (c0 + u < nnz) ? __ldg(skeys + c0 + u) : 0xFFFFFFFEu;
+    nk[0] = (c0 > 0 && c0 <= nnz) ? __ldg(skeys + c0 - 1) : 0xFFFFFFFFu;
+#pragma unroll
+    for (int u = 0; u < CH; ++u) ngv[u] = (c0 + u < nnz) ? __ldg(svals + c0 + u) : 0;
+  };
+  fetch(warp_global * gpw * CH + (int64_t)gin * CH);
+  for (int64_t base = warp_global * gpw * CH; base < nnz; base += stride) {
+    const int64_t c0 = base + (int64_t)gin * CH;
+    uint32_t k[CH + 1];
+    int32_t gv[CH];
+    const uint32_t prev = nk[0];
+#pragma unroll
+    for (int u = 0; u <= CH; ++u) k[u] = nk[u + 1];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) gv[u] = ngv[u];
+    fetch(c0 + stride);
+    bool head[CH];
+    int sh[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      head[u] = (c0 + u < nnz) && k[u] != invalid && k[u] != (u ? k[u - 1] : prev);
+      int lo = 0, hi = nsh - 1;  // last shard with key_base <= key
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (s_kb[mid] <= k[u]) lo = mid; else hi = mid - 1;
+      }
+      sh[u] = lo;
+    }
+    Frag<T, VEC> g0[CH][NV], w[CH][NV];
+#pragma unroll
+    for (int u = 0; u < CH; ++u)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int c = (v * G + t) * VEC;
+        if (head[u] && c < s_w[sh[u]]) {
+          g0[u][v].load(reinterpret_cast<const T*>(gbase + ((int64_t)gv[u] << 4)) + c);
+          w[u][v].load(reinterpret_cast<const T*>(s_wp[sh[u]]) + (int64_t)(k[u] - s_kb[sh[u]]) * s_ld[sh[u]] + c);
+        } else {
+          g0[u][v].zero();
+          w[u][v].zero();
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int width = s_w[sh[u]];
+      A acc[NV][VEC];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[v][e] = A(0);
+        g0[u][v].add_to(acc[v]);
+      }
+      if (head[u] && k[u + 1] == k[u]) {
+        for (int64_t j = c0 + u + 1; j < nnz && __ldg(skeys + j) == k[u]; ++j) {
+          const T* gp = reinterpret_cast<const T*>(gbase + ((int64_t)__ldg(svals + j) << 4));
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const int c = (v * G + t) * VEC;
+            if (c < width) {
+              A x[VEC];
+              Loader<T, VEC>::load(gp + c, x);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) acc[v][e] += x[e];
+            }
+          }
+        }
+      }
+      A step = (A)lr;
+      if (opt == DMT_OPT_ROWWISE_ADAGRAD) {
+        float sq = 0.f;
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) sq += (float)(acc[v][e] * acc[v][e]);
+        for (int o = G >> 1; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o, G);
+        if (head[u]) {
+          float* st = s_st[sh[u]] + (k[u] - s_kb[sh[u]]);
+          const float s_new = *st + sq / (float)width;
+          step = (A)(lr / (sqrtf(s_new) + eps));
+          __syncwarp(__activemask());
+          if (t == 0) *st = s_new;
+        }
+      }
+      if (!head[u]) continue;
+      T* W = const_cast<T*>(reinterpret_cast<const T*>(s_wp[sh[u]])) + (int64_t)(k[u] - s_kb[sh[u]]) * s_ld[sh[u]];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int c = (v * G + t) * VEC;
+        if (c < width) {
+          A nw[VEC];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) nw[e] = A(0);
+          w[u][v].add_to(nw);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) nw[e] = nw[e] - step * acc[v][e];
+          Loader<T, VEC>::store(W + c, nw);
+        }
+      }
+    }
+  }
+}
+
 struct BwdLayout {
   size_t keys_in, keys_out, vals_in, vals_out, recs, cub_temp, total;
   size_t cub_bytes;
@@ -453,6 +620,48 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     if (hs[i].ld > 65535 || hs[i].width > 65535) return DMT_ERR_UNSUPPORTED;
   }
   if (max_b == 0) return DMT_OK;
+  // fast path: no mean pooling, 16-byte aligned gradient rows inside one
+  // buffer (offset < 32 GB), <= kMaxShards distinct shards, vector widths
+  constexpr int VEC0 = Vec16<T>::N;
+  const char* gbase = nullptr;
+  ShardTab tab;
+  tab.n = 0;
+  bool fast = true;
+  for (int i = 0; i < n && fast; ++i) {
+    const dmt_lookup_segment& g = hs[i];
+    if (g.pooling == DMT_POOL_MEAN || (g.out_ld * (int64_t)sizeof(T)) % 16 || ((uintptr_t)g.out & 15) ||
+        g.width % VEC0 || g.ld % VEC0 || ((uintptr_t)g.weights & 15))
+      fast = false;
+    if (!gbase || (const char*)g.out < gbase) gbase = (const char*)g.out;
+  }
+  if (fast) {
+    for (int i = 0; i < n && fast; ++i) {
+      const dmt_lookup_segment& g = hs[i];
+      const int64_t span = ((const char*)g.out - gbase) + (int64_t)g.nbags * g.out_ld * (int64_t)sizeof(T);
+      if (span >= (int64_t(1) << 35)) fast = false;
+      bool seen = false;
+      for (int j = 0; j < tab.n; ++j)
+        if (tab.key_base[j] == (uint32_t)g.key_base) seen = true;
+      if (!seen) {
+        if (tab.n == kMaxShards) { fast = false; break; }
+        int j = tab.n++;
+        tab.key_base[j] = (uint32_t)g.key_base;
+        tab.ld[j] = (uint16_t)g.ld;
+        tab.width[j] = (uint16_t)g.width;
+        tab.weights[j] = (const char*)g.weights;
+        tab.state[j] = (float*)g.state;
+      }
+    }
+    // sort the shard table by key base (insertion sort; tiny)
+    for (int i = 1; i < tab.n; ++i)
+      for (int j = i; j > 0 && tab.key_base[j - 1] > tab.key_base[j]; --j) {
+        std::swap(tab.key_base[j - 1], tab.key_base[j]);
+        std::swap(tab.ld[j - 1], tab.ld[j]);
+        std::swap(tab.width[j - 1], tab.width[j]);
+        std::swap(tab.weights[j - 1], tab.weights[j]);
+        std::swap(tab.state[j - 1], tab.state[j]);
+      }
+  }
   BwdLayout L = bwd_layout(nnz, key_space, nbags);
   if (ws_bytes < L.total) return DMT_ERR_DOMAIN;
   char* w = (char*)ws;
@@ -465,7 +674,11 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
 
   if (phase & 1) {
     dim3 kg((unsigned)ceil_div((int64_t)max_b * 8, 256), n);
-    bwd_keys_kernel<<<kg, 256, 0, s>>>(segs, offsets, indices, invalid, keys_in, vals_in, recs, (int)sizeof(T));
+    if (fast)
+      bwd_keys_fast_kernel<<<kg, 256, 0, s>>>(segs, offsets, indices, invalid, keys_in, vals_in, gbase,
+                                              (int)sizeof(T));
+    else
+      bwd_keys_kernel<<<kg, 256, 0, s>>>(segs, offsets, indices, invalid, keys_in, vals_in, recs, (int)sizeof(T));
     DMT_CHECK_LAUNCH();
     size_t cub_bytes = L.cub_bytes;
     if (cub::DeviceRadixSort::SortPairs((void*)(w + L.cub_temp), cub_bytes, keys_in, keys_out, vals_in, vals_out,
@@ -484,7 +697,25 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     const int gpb = kLookupThreads >> log2g;
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ceil_div(nnz, 4), gpb), (int64_t)DMT_NUM_SMS * 12));
   };
-  if (vec_ok) {
+  if (fast) {
+    // G threads per row with two 16-byte vectors each (NV = 2): twice the rows
+    // per warp of the one-vector layout at the same register cost
+    const int nvec = (max_w + VEC - 1) / VEC;
+    int G = 1, log2g = 0;
+    while (G * 2 < nvec && G < 32) { G <<= 1; ++log2g; }
+    const int nv = (nvec + G - 1) / G;
+    if (nv == 1)
+      bwd_update_fast_kernel<T, VEC, 1, 4><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+    else if (nv == 2)
+      bwd_update_fast_kernel<T, VEC, 2, 2><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+    else if (nv <= 4)
+      bwd_update_fast_kernel<T, VEC, 4, 1><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+    else
+      return DMT_ERR_UNSUPPORTED;
+  } else if (vec_ok) {
     const int nvec = (max_w + VEC - 1) / VEC;
     int G = 1, log2g = 0;
     while (G < nvec && G < 32) { G <<= 1; ++log2g; }
