@@ -216,7 +216,14 @@ enum dmt_epilogue {
  * holds A^T as a [k, m] matrix with row stride lda (m contiguous); TRANS_B:
  * `b` holds B^T as [k, n] with row stride ldb.  Read straight by TMA, no
  * transpose pass (dW = G^T X, dX = G W). */
-enum dmt_gemm_flags { DMT_GEMM_TRANS_A = 1, DMT_GEMM_TRANS_B = 2, DMT_GEMM_AUX2_ACCUM = 4 };
+enum dmt_gemm_flags {
+  DMT_GEMM_TRANS_A = 1,
+  DMT_GEMM_TRANS_B = 2,
+  DMT_GEMM_AUX2_ACCUM = 4,
+  /* acc is scaled by args.alpha before the epilogue: with DMT_EPI_ACC,
+   * beta = 1 and c = d = W this is a fused SGD step W -= lr * dW (alpha = -lr) */
+  DMT_GEMM_SCALE_ACC = 8
+};
 
 typedef struct dmt_gemm_args {
   const void* a;   /* [m, k] row stride lda */
@@ -232,6 +239,7 @@ typedef struct dmt_gemm_args {
   int64_t lda, ldb, ld_d, ld_x;
   int64_t rows_per_group, ld_group;
   float beta;
+  float alpha;       /* with DMT_GEMM_SCALE_ACC */
   int32_t in_dtype;  /* dmt_dtype of a, b (and x0/xl/aux for CROSS) */
   int32_t out_dtype; /* dmt_dtype of d */
   int32_t epilogue;

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libdmt.so")
 DT_F32, DT_BF16, DT_F64, DT_F16 = 0, 1, 2, 3
 POOL_NONE, POOL_SUM, POOL_MEAN = 0, 1, 2
 EPI_NONE, EPI_BIAS, EPI_CROSS, EPI_ACC, EPI_DCN_BWD, EPI_DCN_FINAL = 0, 1, 2, 3, 4, 5
-GEMM_TRANS_A, GEMM_TRANS_B, GEMM_AUX2_ACCUM = 1, 2, 4
+GEMM_TRANS_A, GEMM_TRANS_B, GEMM_AUX2_ACCUM, GEMM_SCALE_ACC = 1, 2, 4, 8
 OPT_SGD, OPT_ROWWISE_ADAGRAD = 0, 1
 EBIT_INDEX, EBIT_BAGLEN = 1, 2
 
@@ -60,7 +60,7 @@ class GemmArgs(C.Structure):
         ("m", i64), ("n", i64), ("k", i64),
         ("lda", i64), ("ldb", i64), ("ld_d", i64), ("ld_x", i64),
         ("rows_per_group", i64), ("ld_group", i64),
-        ("beta", f32), ("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("flags", i32),
+        ("beta", f32), ("alpha", f32), ("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("flags", i32),
     ]
 
 

@@ -130,6 +130,36 @@ __global__ void colsum_partial(const T* __restrict__ in, int64_t rows, int64_t c
   part[(int64_t)blockIdx.y * cols + c] = acc;
 }
 
+// 16-byte vector loads: a warp reads 512 contiguous bytes of a row per step.
+template <typename T>
+__global__ void colsum_partial_vec(const T* __restrict__ in, int64_t rows, int64_t cols, int64_t ld,
+                                   int64_t rows_per, double* __restrict__ part) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
+  if (c >= cols) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
+  float acc[V];
+#pragma unroll
+  for (int e = 0; e < V; ++e) acc[e] = 0.f;
+  double dacc[V];
+#pragma unroll
+  for (int e = 0; e < V; ++e) dacc[e] = 0.0;
+  int cnt = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    uint4 x = __ldg(reinterpret_cast<const uint4*>(in + r * ld + c));
+    const T* h = reinterpret_cast<const T*>(&x);
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[e] += to_f<T>(h[e]);
+    if (++cnt == 32) {  // fold fp32 partial sums into fp64 every 32 rows
+#pragma unroll
+      for (int e = 0; e < V; ++e) { dacc[e] += acc[e]; acc[e] = 0.f; }
+      cnt = 0;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < V; ++e) part[(int64_t)blockIdx.y * cols + c + e] = dacc[e] + acc[e];
+}
+
 __global__ void colsum_final(const double* __restrict__ part, int64_t cols, int nparts, float* __restrict__ out) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
@@ -254,7 +284,7 @@ int dmt_transpose(const void* in, int64_t rows, int64_t cols, int64_t ld_in, voi
 }
 
 static inline int colsum_parts(int64_t rows) {
-  return (int)std::min<int64_t>(std::max<int64_t>(1, rows / 256), 64);
+  return (int)std::min<int64_t>(std::max<int64_t>(1, rows / 64), 256);
 }
 
 size_t dmt_column_sum_workspace_size(int64_t rows, int64_t cols) {
@@ -269,6 +299,23 @@ int dmt_column_sum(const void* in, int64_t rows, int64_t cols, int64_t ld, float
   int64_t rows_per = dmt::ceil_div(std::max<int64_t>(rows, 1), nparts);
   if (workspace_bytes < dmt_column_sum_workspace_size(rows, cols)) return DMT_ERR_DOMAIN;
   double* g_colsum_scratch = (double*)workspace;
+  const size_t es = dmt::dtype_size(dtype);
+  const bool vec = es && es <= 4 && dtype != DMT_F64 && ((uintptr_t)in % 16 == 0) && ((ld * es) % 16 == 0) &&
+                   ((cols * es) % 16 == 0);
+  if (vec) {
+    const int V = 16 / (int)es;
+    dim3 vg((unsigned)dmt::ceil_div(cols / V, 128), nparts);
+    if (dtype == DMT_F32)
+      dmt::colsum_partial_vec<float><<<vg, 128, 0, s>>>((const float*)in, rows, cols, ld, rows_per, g_colsum_scratch);
+    else if (dtype == DMT_BF16)
+      dmt::colsum_partial_vec<__nv_bfloat16><<<vg, 128, 0, s>>>((const __nv_bfloat16*)in, rows, cols, ld, rows_per,
+                                                                g_colsum_scratch);
+    else
+      dmt::colsum_partial_vec<__half><<<vg, 128, 0, s>>>((const __half*)in, rows, cols, ld, rows_per, g_colsum_scratch);
+    dmt::colsum_final<<<(unsigned)dmt::ceil_div(cols, 256), 256, 0, s>>>(g_colsum_scratch, cols, nparts, out);
+    DMT_CHECK_LAUNCH();
+    return DMT_OK;
+  }
   dim3 grid((unsigned)dmt::ceil_div(cols, 256), nparts);
   switch (dtype) {
     case DMT_F32: dmt::colsum_partial<float><<<grid, 256, 0, s>>>((const float*)in, rows, cols, ld, rows_per, g_colsum_scratch); break;

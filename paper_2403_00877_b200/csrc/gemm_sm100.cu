@@ -177,6 +177,8 @@ struct Params {
   const void* c;
   float* aux2;
   float beta;
+  float alpha;
+  int scale_acc;
   int aux2_accum;
   int out_dtype;
   int in_dtype;
@@ -540,6 +542,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       for (int c = half * kColsPerWarp; c < (half + 1) * kColsPerWarp; c += 32) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), v);
+        if (p.scale_acc) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
+        }
         const int64_t col = n0 + c;
         const int64_t rem = p.n - col;
         const int ncols = rem <= 0 ? 0 : (rem < 32 ? (int)rem : 32);
@@ -739,6 +745,8 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   p.c = a->c ? a->c : a->d;
   p.aux2 = a->aux2;
   p.aux2_accum = (a->flags & DMT_GEMM_AUX2_ACCUM) != 0;
+  p.scale_acc = (a->flags & DMT_GEMM_SCALE_ACC) != 0;
+  p.alpha = a->alpha;
   p.beta = a->beta; p.out_dtype = a->out_dtype; p.in_dtype = a->in_dtype; p.epilogue = a->epilogue;
   size_t eo = dtype_size(a->out_dtype);
   p.vec_store = ((uintptr_t)a->d % 16 == 0) && ((a->ld_d * eo) % 16 == 0) && ((a->ld_group * eo) % 16 == 0);

@@ -327,7 +327,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[
          epilogue: int = L.EPI_NONE, x0=None, xl=None, aux=None, beta: float = 0.0,
          rows_per_group: int = 0, ld_group: int = 0, ld_d: Optional[int] = None,
          b_split=None, trans_a: bool = False, trans_b: bool = False, c=None, aux2=None,
-         aux2_accum: bool = False) -> torch.Tensor:
+         aux2_accum: bool = False, alpha: Optional[float] = None) -> torch.Tensor:
     """out[m, n] = epi(sum_k A[m, k] B[n, k]) on tcgen05 (bf16/f16 -> kind::f16,
     fp32 -> 3xTF32).  A = a (m, k), or a^T when ``trans_a`` (a stored (k, m));
     B = b (n, k), or b^T when ``trans_b`` (b stored (k, n)).  Transposed
@@ -367,14 +367,15 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[
     if bias is not None and (bias.dtype != torch.float32 or not bias.is_contiguous()):
         bias = bias.float().contiguous()
     flags = ((L.GEMM_TRANS_A if trans_a else 0) | (L.GEMM_TRANS_B if trans_b else 0)
-             | (L.GEMM_AUX2_ACCUM if aux2_accum else 0))
+             | (L.GEMM_AUX2_ACCUM if aux2_accum else 0) | (L.GEMM_SCALE_ACC if alpha is not None else 0))
     args = L.GemmArgs(
         a=a.data_ptr(), b=b.data_ptr(), d=out.data_ptr(), bias=L.ptr(bias), x0=L.ptr(x0), xl=L.ptr(xl),
         aux=L.ptr(aux), c=L.ptr(c), aux2=L.ptr(aux2), m=m, n=n, k=k, lda=a.stride(0), ldb=b.stride(0),
         ld_d=ld_d if ld_d is not None else out.stride(0),
         ld_x=(x0.stride(0) if x0 is not None else (aux2.stride(0) if aux2 is not None else 0)),
         rows_per_group=rows_per_group, ld_group=ld_group,
-        beta=beta, in_dtype=in_dt, out_dtype=_dt(out), epilogue=epilogue, flags=flags)
+        beta=beta, alpha=alpha if alpha is not None else 1.0, in_dtype=in_dt, out_dtype=_dt(out),
+        epilogue=epilogue, flags=flags)
     L.check(L.lib().dmt_gemm_ex(C.byref(args), L.ptr(a_lo), L.ptr(b_lo), L.stream_ptr()), "dmt_gemm")
     return out
 

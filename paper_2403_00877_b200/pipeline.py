@@ -397,8 +397,11 @@ class SpttEngine:
             t = p.tower_of(r)
             if t in self.tm:
                 self.tm[t]._saved = self.buf[r]["tm_saved"]
+                # a one-rank tower needs no gradient all-reduce: fuse the weight
+                # SGD into the dW GEMM epilogues
+                fused = (tm_lr if tm_lr is not None else lr) if p.W == 1 else None
                 with self._t("tm_bwd"):
-                    dX[r] = self.tm[t].backward(grecv[r])
+                    dX[r] = self.tm[t].backward(grecv[r], fused_lr=fused)
                 acc = tower_grads.setdefault(t, {})
                 for k, v in self.tm[t].grads.items():
                     acc[k] = v.clone() if k not in acc else acc[k].add_(v)

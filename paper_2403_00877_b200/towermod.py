@@ -226,14 +226,19 @@ class TowerModule:
                    rows_per_group=self.F, ld_group=O, ld_d=cD)
 
     # -- backward --------------------------------------------------------------
-    def backward(self, gy: torch.Tensor) -> torch.Tensor:
+    def backward(self, gy: torch.Tensor, fused_lr: Optional[float] = None) -> torch.Tensor:
         """Returns dX (rows, F*N) in the compute dtype; fp32 weight grads are
-        stored in ``self.grads`` (this rank's contribution only)."""
+        stored in ``self.grads`` (this rank's contribution only).
+
+        ``fused_lr``: when no cross-rank gradient reduction is needed (a tower
+        of one rank), the DCN weight matrices are updated in place by the dW
+        GEMM epilogue (W -= lr * dW, dmt_gemm SCALE_ACC + ACC) and only the
+        bias grads are left in ``self.grads``."""
         if self._saved is None:
             raise DomainError("backward() needs forward(save=True)")
         if self.cfg.kind == DLRM:
             return self._dlrm_bwd(gy)
-        return self._dcn_bwd(gy)
+        return self._dcn_bwd(gy, fused_lr)
 
     def _dlrm_bwd(self, gy):
         (x,) = self._saved
@@ -278,37 +283,47 @@ class TowerModule:
             dx.zero_()
         return dx
 
-    def _dcn_bwd(self, gy):
+    def _dcn_bwd(self, gy, fused_lr: Optional[float] = None):
         """Crossnet backward with the element-wise work fused into GEMM
         epilogues (dmt_gemm DCN_BWD / DCN_FINAL):
             g_L = gy Wp;  gu_l = g_{l+1} * x0;  dx0 += g_{l+1} * u_l
             dW_l = gu_l^T x_l;  g_l = gu_l W_l + g_{l+1};  dX = g_0 + dx0
-        (derivative of towermod.py:132-158; x_0 = X, u_l = x_l W_l^T + b_l)."""
+        (derivative of towermod.py:132-158; x_0 = X, u_l = x_l W_l^T + b_l).
+        Each dX-side GEMM runs before the weight it reads is (optionally)
+        updated in place."""
         xs, us = self._saved
         x0 = xs[0]
         rows, M = x0.shape
         L_ = self.cfg.cross_layers
         f32 = torch.float32
         dev = x0.device
-        self.grads["w_proj"] = K.gemm(gy, xs[-1], torch.empty(self.w["w_proj"].shape, dtype=f32, device=dev),
-                                      trans_a=True, trans_b=True)
-        self.grads["b_proj"] = K.column_sum(gy)
+        self.grads = {}
+
+        def weight_grad(name, a, b):
+            if fused_lr is not None:  # W -= lr * a^T b, in the GEMM epilogue
+                K.gemm(a, b, self.w[name], trans_a=True, trans_b=True, epilogue=L.EPI_ACC, beta=1.0,
+                       alpha=-fused_lr)
+            else:
+                self.grads[name] = K.gemm(a, b, torch.empty(self.w[name].shape, dtype=f32, device=dev),
+                                          trans_a=True, trans_b=True)
+
         g = torch.empty((rows, M), dtype=self.dtype, device=dev)
         gu = [torch.empty((rows, M), dtype=self.dtype, device=dev) for _ in range(2)]
         dx0 = torch.empty((rows, M), dtype=f32, device=dev)
         K.gemm(gy, self.w["w_proj"], g, trans_b=True, epilogue=L.EPI_DCN_BWD, x0=x0, xl=us[L_ - 1],
                aux=gu[(L_ - 1) % 2], aux2=dx0, aux2_accum=False)
+        weight_grad("w_proj", gy, xs[-1])
+        self.grads["b_proj"] = K.column_sum(gy)
         dx = torch.empty_like(g)
         for layer in range(L_ - 1, -1, -1):
             cur = gu[layer % 2]
-            self.grads[f"w{layer}"] = K.gemm(cur, xs[layer], torch.empty((M, M), dtype=f32, device=dev),
-                                             trans_a=True, trans_b=True)
-            self.grads[f"b{layer}"] = K.column_sum(cur)
             if layer > 0:
                 K.gemm(cur, self.w[f"w{layer}"], g, trans_b=True, epilogue=L.EPI_DCN_BWD, c=g, beta=1.0, x0=x0,
                        xl=us[layer - 1], aux=gu[(layer - 1) % 2], aux2=dx0, aux2_accum=True)
             else:
                 K.gemm(cur, self.w["w0"], dx, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=g, beta=1.0, aux2=dx0)
+            weight_grad(f"w{layer}", cur, xs[layer])
+            self.grads[f"b{layer}"] = K.column_sum(cur)
         return dx
 
     def sgd_step(self, lr: float) -> None:

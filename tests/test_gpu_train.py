@@ -192,3 +192,24 @@ def test_sptt_train_step_loopback_vs_oracle(hosts, rph, kind):
     for sid, sh in enumerate(placement.shards):
         got = model.engine.weights[sid].double().cpu().numpy()
         np.testing.assert_allclose(got, expect[sh.table_id], rtol=1e-4, atol=2e-5)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+def test_dcn_fused_sgd_matches_unfused(dt):
+    """W -= lr * dW inside the dW GEMM epilogue == explicit grads + SGD."""
+    F, N, rows, lr = 4, 32, 256, 0.05
+    tm_a, _, _ = _tm_objects("dcn", F, N, dt, seed=3)
+    tm_b, _, _ = _tm_objects("dcn", F, N, dt, seed=3)
+    rng = np.random.default_rng(8)
+    x = torch.from_numpy(rng.normal(size=(rows, F * N)) * 0.5).to(dev(), dt)
+    g = torch.from_numpy(rng.normal(size=(rows, tm_a.width))).to(dev(), dt)
+    tm_a.forward(x, save=True)
+    dxa = tm_a.backward(g)
+    tm_a.sgd_step(lr)
+    tm_b.forward(x, save=True)
+    dxb = tm_b.backward(g, fused_lr=lr)
+    tm_b.sgd_step(lr)  # biases only
+    tol = 1e-5 if dt == torch.float32 else 2e-2
+    assert torch.allclose(dxa.double(), dxb.double(), rtol=tol, atol=tol)
+    for k in tm_a.w:
+        assert torch.allclose(tm_a.w[k].double(), tm_b.w[k].double(), rtol=tol, atol=tol), k
