@@ -567,6 +567,259 @@ bwd_update_fast_kernel(const uint32_t* __restrict__ skeys, const int32_t* __rest
   }
 }
 
+// ---- asynchronous-copy variant of the fast path ----------------------------
+// Each warp owns chunks of R = 256 / NVEC sorted occurrences.  For a chunk it
+// resolves keys, run heads and row addresses (lane = occurrence), then streams
+// the gradient rows of all its occurrences and the weight rows of its run
+// heads into a 3-deep shared-memory ring with cp.async (16 B per request, no
+// registers held while in flight), so ~2 chunks per warp stay in flight.  The
+// update reads both from shared memory; a run that continues past the chunk
+// end is finished with direct loads (rare for uniform indices).
+constexpr int kAsyncWarps = 8;
+constexpr int kAsyncStages = 3;
+constexpr int kAsyncVecs = 256;  // 16-byte vectors per array per chunk (4 KB)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(smem)),
+      "l"(gmem), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+struct ChunkMeta {
+  uint32_t key;
+  int32_t head;
+  const char* grad;
+  char* wrow;
+  float* srow;
+};
+
+template <typename T, int NVEC>
+__global__ void __launch_bounds__(kAsyncWarps * 32, 1)
+bwd_update_async_kernel(const uint32_t* __restrict__ skeys, const int32_t* __restrict__ svals, int64_t nnz,
+                        const char* __restrict__ gbase, const __grid_constant__ ShardTab tab, uint32_t invalid,
+                        int opt, float lr, float eps) {
+  using A = typename Acc<T>::type;
+  constexpr int R = kAsyncVecs / NVEC;          // occurrences per chunk (<= 32)
+  constexpr int VEC = 16 / sizeof(T);           // elements per vector
+  constexpr int RPS = 32 / NVEC;                // rows processed per warp step
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint4* ring = reinterpret_cast<uint4*>(smem_raw);  // [warps][stages][2][256] x 16 B
+  ChunkMeta* meta_all = reinterpret_cast<ChunkMeta*>(smem_raw + (size_t)kAsyncWarps * kAsyncStages * 2 *
+                                                                    kAsyncVecs * 16);
+  uint64_t* bars_all = reinterpret_cast<uint64_t*>(meta_all + (size_t)kAsyncWarps * kAsyncStages * (R + 1));
+  __shared__ uint32_t s_kb[kMaxShards];
+  __shared__ uint16_t s_ld[kMaxShards];
+  __shared__ const char* s_wp[kMaxShards];
+  __shared__ float* s_st[kMaxShards];
+  for (int i = threadIdx.x; i < tab.n; i += blockDim.x) {
+    s_kb[i] = tab.key_base[i];
+    s_ld[i] = tab.ld[i];
+    s_wp[i] = tab.weights[i];
+    s_st[i] = tab.state[i];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint4* wring = ring + (size_t)warp * kAsyncStages * 2 * kAsyncVecs;
+  ChunkMeta* wmeta = meta_all + (size_t)warp * kAsyncStages * (R + 1);
+  uint64_t* wbars = bars_all + warp * kAsyncStages;
+  if (lane < kAsyncStages) mbar_init1(&wbars[lane]);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  uint32_t parity_bits = 0;  // per-stage phase parity
+  const int64_t nchunks = ceil_div(nnz, R);
+  const int64_t wstride = (int64_t)gridDim.x * kAsyncWarps;
+  const int64_t first = (int64_t)blockIdx.x * kAsyncWarps + warp;
+
+  // keys / values of a chunk are fetched into registers one chunk ahead of the
+  // resolve + copy issue, so their latency overlaps the previous chunk's work
+  uint32_t rk = 0, rkp = 0;
+  int32_t rgv = 0;
+  int64_t rc = -1;
+  auto fetch = [&](int64_t c) {
+    rc = c;
+    if (c < nchunks && lane <= R) {
+      const int64_t pos = c * R + lane;
+      rk = pos < nnz ? __ldg(skeys + pos) : 0xFFFFFFFEu;
+      rkp = pos > 0 && pos <= nnz ? __ldg(skeys + pos - 1) : 0xFFFFFFFFu;
+      rgv = (lane < R && pos < nnz) ? __ldg(svals + pos) : 0;
+    }
+  };
+  // resolve the fetched chunk into stage `st` and issue its copies (one group)
+  auto issue = [&](int st) {
+    ChunkMeta* m = wmeta + st * (R + 1);
+    const int64_t c = rc;
+    if (c < nchunks) {
+      const int64_t pos = c * R + lane;
+      if (lane <= R) {
+        const uint32_t k = rk;
+        ChunkMeta mm;
+        mm.key = k;
+        mm.head = (lane < R && pos < nnz && k != invalid && k != rkp) ? 1 : 0;
+        mm.grad = (lane < R && pos < nnz) ? gbase + ((int64_t)rgv << 4) : nullptr;
+        mm.wrow = nullptr;
+        mm.srow = nullptr;
+        if (mm.head) {
+          int lo = 0, hi = tab.n - 1;
+          while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (s_kb[mid] <= k) lo = mid; else hi = mid - 1;
+          }
+          const int64_t row = (int64_t)(k - s_kb[lo]);
+          mm.wrow = const_cast<char*>(s_wp[lo]) + row * s_ld[lo] * (int64_t)sizeof(T);
+          mm.srow = s_st[lo] ? s_st[lo] + row : nullptr;
+        }
+        m[lane] = mm;
+      }
+      __syncwarp();
+      // one bulk (TMA) copy per row and array, issued by the row's own lane
+      uint4* gbuf = wring + (size_t)st * 2 * kAsyncVecs;
+      uint4* wbuf = gbuf + kAsyncVecs;
+      constexpr uint32_t RB = NVEC * 16;
+      uint32_t mine = 0;
+      if (lane < R) {
+        const ChunkMeta& mi = m[lane];
+        if (mi.grad && mi.key != invalid) {
+          bulk_g2s(gbuf + lane * NVEC, mi.grad, RB, &wbars[st]);
+          mine += RB;
+        }
+        if (mi.head) {
+          bulk_g2s(wbuf + lane * NVEC, mi.wrow, RB, &wbars[st]);
+          mine += RB;
+        }
+      }
+      const uint32_t total = __reduce_add_sync(0xffffffffu, mine);
+      if (lane == 0) mbar_arrive_tx(&wbars[st], total);
+    } else if (lane == 0) {
+      mbar_arrive_tx(&wbars[st], 0);  // keep the stage's phase sequence uniform
+    }
+  };
+
+  int64_t c = first;
+  fetch(c);
+  issue(0);
+  fetch(c + wstride);
+  issue(1);
+  fetch(c + 2 * wstride);
+  for (int st = 0; c < nchunks; c += wstride, st = (st + 1) % kAsyncStages) {
+    issue((st + 2) % kAsyncStages);  // chunk c + 2*stride (keys fetched last iteration)
+    fetch(c + 3 * wstride);          // keys of chunk c + 3*stride, consumed next iteration
+    mbar_wait_parity(&wbars[st], (parity_bits >> st) & 1u);
+    parity_bits ^= 1u << st;
+    __syncwarp();
+    const ChunkMeta* m = wmeta + st * (R + 1);
+    const uint4* gbuf = wring + (size_t)st * 2 * kAsyncVecs;
+    const uint4* wbuf = gbuf + kAsyncVecs;
+    const int64_t p0 = c * R;
+    const int sub = lane / NVEC, v = lane % NVEC;
+#pragma unroll 1
+    for (int s = 0; s < R; s += RPS) {
+      const int i = s + sub;
+      const ChunkMeta mi = m[i];
+      A acc[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] = A(0);
+      if (mi.head) {
+        Frag<T, VEC> f;
+        f.r = *reinterpret_cast<const typename Frag<T, VEC>::Raw*>(&gbuf[i * NVEC + v]);
+        f.add_to(acc);
+        int q = i + 1;
+        for (; q < R && m[q].key == mi.key; ++q) {
+          Frag<T, VEC> f2;
+          f2.r = *reinterpret_cast<const typename Frag<T, VEC>::Raw*>(&gbuf[q * NVEC + v]);
+          f2.add_to(acc);
+        }
+        if (q == R) {  // the run may continue into the next chunk(s)
+          for (int64_t j = p0 + R; j < nnz && __ldg(skeys + j) == mi.key; ++j) {
+            A x[VEC];
+            Loader<T, VEC>::load(reinterpret_cast<const T*>(gbase + ((int64_t)__ldg(svals + j) << 4)) + v * VEC, x);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[e] += x[e];
+          }
+        }
+      }
+      A step = (A)lr;
+      if (opt == DMT_OPT_ROWWISE_ADAGRAD) {
+        float sq = 0.f;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) sq += (float)(acc[e] * acc[e]);
+        for (int o = NVEC >> 1; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o, NVEC);
+        if (mi.head) {
+          const float s_new = *mi.srow + sq / (float)(NVEC * VEC);
+          step = (A)(lr / (sqrtf(s_new) + eps));
+          __syncwarp(__activemask());
+          if (v == 0) *mi.srow = s_new;
+        }
+      }
+      if (mi.head) {
+        Frag<T, VEC> wf;
+        wf.r = *reinterpret_cast<const typename Frag<T, VEC>::Raw*>(&wbuf[i * NVEC + v]);
+        A nw[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) nw[e] = A(0);
+        wf.add_to(nw);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) nw[e] = nw[e] - step * acc[e];
+        Loader<T, VEC>::store(reinterpret_cast<T*>(mi.wrow) + v * VEC, nw);
+      }
+    }
+    __syncwarp();
+  }
+  // stages issued past the last chunk carry no copies (0-byte arrivals)
+}
+
+template <typename T, int NVEC>
+int launch_async_update(const uint32_t* keys, const int32_t* vals, int64_t nnz, const char* gbase,
+                        const ShardTab& tab, uint32_t invalid, int opt, float lr, float eps, cudaStream_t s) {
+  constexpr int R = kAsyncVecs / NVEC;
+  const size_t smem = (size_t)kAsyncWarps * kAsyncStages * 2 * kAsyncVecs * 16 +
+                      (size_t)kAsyncWarps * kAsyncStages * (R + 1) * sizeof(ChunkMeta) +
+                      (size_t)kAsyncWarps * kAsyncStages * 8;
+  auto kern = bwd_update_async_kernel<T, NVEC>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return DMT_ERR_CUDA;
+    attr = true;
+  }
+  const int64_t nchunks = ceil_div(nnz, R);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nchunks, kAsyncWarps),
+                                                                          DMT_NUM_SMS));
+  kern<<<grid, kAsyncWarps * 32, smem, s>>>(keys, vals, nnz, gbase, tab, invalid, opt, lr, eps);
+  return DMT_OK;
+}
+
 struct BwdLayout {
   size_t keys_in, keys_out, vals_in, vals_out, recs, cub_temp, total;
   size_t cub_bytes;
@@ -697,6 +950,25 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     const int gpb = kLookupThreads >> log2g;
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ceil_div(nnz, 4), gpb), (int64_t)DMT_NUM_SMS * 12));
   };
+  const int nvec_all = (max_w + VEC - 1) / VEC;
+  // 4/8-byte rows: bulk-copy (TMA) staged kernel; 16-bit rows keep the
+  // register-resident kernel below (measured faster for bf16 at C2)
+  if (fast && sizeof(T) >= 4 && nvec_all * VEC == max_w && (nvec_all == 8 || nvec_all == 16 || nvec_all == 32)) {
+    bool uniform_w = true;
+    for (int i = 0; i < n; ++i) uniform_w = uniform_w && hs[i].width == max_w;
+    if (uniform_w) {
+      int rc;
+      if (nvec_all == 8)
+        rc = launch_async_update<T, 8>(keys_out, vals_out, nnz, gbase, tab, invalid, opt, lr, eps, s);
+      else if (nvec_all == 16)
+        rc = launch_async_update<T, 16>(keys_out, vals_out, nnz, gbase, tab, invalid, opt, lr, eps, s);
+      else
+        rc = launch_async_update<T, 32>(keys_out, vals_out, nnz, gbase, tab, invalid, opt, lr, eps, s);
+      if (rc != DMT_OK) return rc;
+      DMT_CHECK_LAUNCH();
+      return DMT_OK;
+    }
+  }
   if (fast) {
     // G threads per row with two 16-byte vectors each (NV = 2): twice the rows
     // per warp of the one-vector layout at the same register cost
