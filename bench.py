@@ -32,7 +32,7 @@ UNIT = "samples/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dmt", choices=["dmt", "reference"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
@@ -69,7 +69,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -281,13 +281,13 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    def timed_graph(m, K, host_inputs=None):
+    def timed_graph(m, K, host_inputs=None, timers=None):
         """The timed region: K CUDA-graph replays of the whole train step.  Each
         step first copies its batch into the graph's static input buffers
         (device->device, or pinned host->device for e2e) inside the region."""
         st = {rank: KJT(batches[0][rank].lengths.clone(), batches[0][rank].values.clone(),
                         batches[0][rank].nnz_per_feature, B)}
-        replay, outs = m.capture(st, gout)
+        replay, outs = m.capture(st, gout, timers=timers)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
@@ -348,11 +348,16 @@ def main():
     # per-phase breakdown (eager, instrumented) -- also the fallback timing
     eager_ms, timers, calls = timed_eager(model, args.steps, args.warmup)
     ph = {k: v / args.steps for k, v in timers.ms().items()}
+    ph_source = "eager"
     graph_ok = True
     clocks = ClockSampler(local)
     clocks.start()
+    gtimers = PhaseTimers(external=True)
     try:
-        total_ms = timed_graph(model, args.steps)
+        total_ms = timed_graph(model, args.steps, timers=gtimers)
+        # phases of the last replay (events are graph nodes, re-recorded each replay)
+        ph = {k: v for k, v in gtimers.ms().items()}
+        ph_source = "cuda-graph replay"
     except Exception as ex:  # capture unsupported (e.g. collective backend): eager numbers
         graph_ok = False
         graph_err = repr(ex)[:200]
@@ -416,7 +421,7 @@ def main():
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic (uniform random rows, random-init tables and TM weights)",
         "config": _config(args, N), "roofline": roof, "roofline_lookup": roof_lookup,
-        "lookup_hbm_gbs": look_gbs, "phases_ms_per_step": ph, "cuda_graph": graph_ok,
+        "lookup_hbm_gbs": look_gbs, "phases_ms_per_step": ph, "phases_source": ph_source, "cuda_graph": graph_ok,
         "eager_ms_per_step": max_over_ranks(eager_ms) / args.steps,
         "exposed_comm_ms_per_step": ph.get("exchange", 0.0), "clocks": clk, "e2e": e2e,
         "gpu_launches": calls * args.steps,
@@ -432,7 +437,10 @@ def main():
         fe_ms, f_t, _ = timed_eager(flat, args.steps, args.warmup)
         fph = {k: v / args.steps for k, v in f_t.ms().items()}
         try:
-            f_ms = timed_graph(flat, args.steps) if graph_ok else max_over_ranks(fe_ms)
+            ft = PhaseTimers(external=True)
+            f_ms = timed_graph(flat, args.steps, timers=ft) if graph_ok else max_over_ranks(fe_ms)
+            if graph_ok:
+                fph = {k: v for k, v in ft.ms().items()}
         except Exception:
             f_ms = max_over_ranks(fe_ms)
         result["flat_baseline"] = {"value": N * B * args.steps / (f_ms / 1000.0), "ms_per_step": f_ms / args.steps,

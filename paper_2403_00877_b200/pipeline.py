@@ -37,10 +37,13 @@ from .simnet import CommTrace
 
 class PhaseTimers:
     """CUDA events around pipeline phases, on the stream the kernels run on
-    (the current stream), for the bench's per-kernel roofline."""
+    (the current stream), for the bench's per-kernel roofline.  With
+    ``external=True`` the events are recorded as CUDA-graph nodes, so a
+    captured step reports its phases on every replay."""
 
-    def __init__(self):
+    def __init__(self, external: bool = False):
         self.events: dict = {}
+        self.external = external
 
     def scope(self, name: str):
         return _Scope(self, name)
@@ -49,7 +52,11 @@ class PhaseTimers:
         self.events = {}
 
     def ms(self) -> dict:
-        return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.events.items()}
+        out = {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.events.items()}
+        ex = [v for k, v in out.items() if k.startswith("exchange_")]
+        if ex:
+            out["exchange"] = sum(ex)
+        return out
 
     def count(self, name: str) -> int:
         return len(self.events.get(name, ()))
@@ -61,13 +68,13 @@ class _Scope:
 
     def __enter__(self):
         if self.t is not None:
-            self.a = torch.cuda.Event(enable_timing=True)
+            self.a = torch.cuda.Event(enable_timing=True, external=self.t.external)
             self.a.record()
         return self
 
     def __exit__(self, *exc):
         if self.t is not None:
-            b = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True, external=self.t.external)
             b.record()
             self.t.events.setdefault(self.name, []).append((self.a, b))
         return False
@@ -243,7 +250,7 @@ class SpttEngine:
             # step is CUDA-graph capturable)
             recv_val_splits = {r: [val_splits[r][r]] * p.G for r in self.local}
         else:
-            with self._t("exchange"):
+            with self._t("exchange_counts"):
                 recv_val_splits = fab.exchange_counts(world, val_splits)
         recv_len, recv_val = {}, {}
         for r in self.local:
@@ -252,10 +259,10 @@ class SpttEngine:
                 continue
             recv_len[r] = torch.empty(max(1, p.owner_bags(r)), dtype=torch.int32, device=dev)
             recv_val[r] = torch.empty(max(1, sum(recv_val_splits[r])), dtype=torch.int32, device=dev)
-        with self._t("exchange"):
+        with self._t("exchange_a_len"):
             fab.alltoallv(world, "a_len", send_len, len_splits, recv_len,
                           {r: [p.S[r] * p.B] * p.G for r in self.local})
-        with self._t("exchange"):
+        with self._t("exchange_a"):
             fab.alltoallv(world, "a", send_val, val_splits, recv_val, recv_val_splits, self.trace, 4)
         # step b: lookup (+ fused permute) on every owner
         self._owner = {}
@@ -285,7 +292,7 @@ class SpttEngine:
         recv = {r: self.buf[r]["recv_d"] for r in self.local}
         for g in self._groups(p.group_of):
             self._trace_d(g)
-            with self._t("exchange"):
+            with self._t("exchange_d"):
                 fab.alltoallv(g, "d", send, {r: p.d_send_splits(r) for r in g}, recv,
                               {r: p.d_recv_splits(r) for r in g}, None)
         # step e: regroup + tower module
@@ -301,7 +308,7 @@ class SpttEngine:
         send = {r: self.buf[r]["Y"].view(-1) for r in self.local}
         recv = {r: self.buf[r]["recv_f"] for r in self.local}
         for g in self._groups(p.class_group_of):
-            with self._t("exchange"):
+            with self._t("exchange_f"):
                 fab.alltoallv(g, "f", send, {r: p.f_send_splits(r) for r in g}, recv,
                               {r: p.f_recv_splits(r) for r in g}, self.trace, self.es)
         out = {}
@@ -315,7 +322,7 @@ class SpttEngine:
         world = list(range(p.G))
         send = {r: self.buf[r]["send_x"] for r in self.local}
         recv = {r: self.buf[r]["recv_c"] for r in self.local}
-        with self._t("exchange"):
+        with self._t("exchange_c"):
             fab.alltoallv(world, "c", send, {r: p.c_send_splits(r) for r in world}, recv,
                           {r: p.c_recv_splits(r) for r in world}, self.trace, self.es)
         out = {}
@@ -365,11 +372,11 @@ class SpttEngine:
 
     # --------------------------------------------------------- backward ----
     def backward(self, grad_out: dict, lr: float, optimizer: int = L.OPT_SGD, eps: float = 1e-8,
-                 tm_lr: Optional[float] = None) -> None:
+                 tm_lr: Optional[float] = None, dense_hook=None) -> None:
         """Backward of the last forward(save=True) + fused optimizer updates."""
         p, fab, dev = self.plan, self.fabric, self.device
         if self.mode == "flat":
-            return self._flat_backward(grad_out, lr, optimizer, eps)
+            return self._flat_backward(grad_out, lr, optimizer, eps, dense_hook)
         # f^-1: pack the tower-grouped gradient into per-tower blocks (the step-f
         # receive layout), send each block back to the member that produced it
         gsend, grecv = {}, {}
@@ -387,7 +394,7 @@ class SpttEngine:
             grecv[r] = (gf.view(p.T * p.B, p.O[p.tower_of(r)]) if p.T == 1 else
                         self._persist(r, "g_y", self.buf[r]["Y"]))
         for g in self._groups(p.class_group_of):
-            with self._t("exchange"):
+            with self._t("exchange_f_bwd"):
                 fab.alltoallv(g, "f_bwd", gsend, {r: p.f_recv_splits(r) for r in g}, {r: grecv[r].view(-1) for r in self.local},
                               {r: p.f_send_splits(r) for r in g})
         # e^-1: tower module backward (weight grads summed over the tower)
@@ -407,12 +414,6 @@ class SpttEngine:
                     acc[k] = v.clone() if k not in acc else acc[k].add_(v)
             else:
                 dX[r] = grecv[r]
-        for t, grads in tower_grads.items():
-            group = p.layout.tower_ranks(t, p.topo)
-            with self._t("exchange"):
-                fab.all_reduce_(group, grads)
-            self.tm[t].grads = grads
-            self.tm[t].sgd_step(tm_lr if tm_lr is not None else lr)
         # d^-1: scatter dX columns back into the step-d receive layout
         dsend, drecv = {}, {}
         for r in self.local:
@@ -426,12 +427,38 @@ class SpttEngine:
             dsend[r] = gd
             drecv[r] = self.buf[r]["grad_x"]
         for g in self._groups(p.group_of):
-            with self._t("exchange"):
+            with self._t("exchange_d_bwd"):
                 fab.alltoallv(g, "d_bwd", dsend, {r: p.d_recv_splits(r) for r in g}, drecv,
                               {r: p.d_send_splits(r) for r in g})
-        self._embedding_update(lr, optimizer, eps)
 
-    def _flat_backward(self, grad_out, lr, optimizer, eps):
+        def tm_reduce_and_step():
+            for t, grads in tower_grads.items():
+                group = p.layout.tower_ranks(t, p.topo)
+                fab.all_reduce_(group, grads)
+                self.tm[t].grads = grads
+                self.tm[t].sgd_step(tm_lr if tm_lr is not None else lr)
+
+        self.overlap_with_embedding_update(tm_reduce_and_step, lr, optimizer, eps)
+
+    def overlap_with_embedding_update(self, fn, lr, optimizer, eps) -> None:
+        """Run ``fn`` (dense-gradient all-reduce + SGD) on a side stream while the
+        fused embedding update runs on the current one.  ``fn``'s collectives are
+        enqueued after the backward all-to-alls on the same communicators, so
+        they execute while the (HBM-bound) update kernel runs."""
+        side = self._side_stream2()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with self._t("overlapped_allreduce"):  # not exposed: hidden under the update
+                fn()
+        self._embedding_update(lr, optimizer, eps)
+        torch.cuda.current_stream().wait_stream(side)
+
+    def _side_stream2(self):
+        if getattr(self, "_side2", None) is None:
+            self._side2 = torch.cuda.Stream(device=self.device)
+        return self._side2
+
+    def _flat_backward(self, grad_out, lr, optimizer, eps, dense_hook=None):
         p, fab, dev = self.plan, self.fabric, self.device
         world = list(range(p.G))
         gsend = {}
@@ -444,10 +471,13 @@ class SpttEngine:
                     copies.append((grad_out[r], fb.dst_col + pc.c0, fw, gc, pc.offset, pc.ld, p.B, pc.width))
             K.Copy2DTable(copies, dev).run()
             gsend[r] = gc
-        with self._t("exchange"):
+        with self._t("exchange_c_bwd"):
             fab.alltoallv(world, "c_bwd", gsend, {r: p.c_recv_splits(r) for r in world},
                           {r: self.buf[r]["grad_x"] for r in self.local}, {r: p.c_send_splits(r) for r in world})
-        self._embedding_update(lr, optimizer, eps)
+        if dense_hook is None:
+            self._embedding_update(lr, optimizer, eps)
+        else:
+            self.overlap_with_embedding_update(dense_hook, lr, optimizer, eps)
 
     def _side_stream(self):
         if self._side is None:

@@ -98,18 +98,20 @@ class SPTT:
                 dx[r] = self.global_tm.backward(g)
             for k, v in self.global_tm.grads.items():
                 acc[k] = v.clone() if k not in acc else acc[k].add_(v)
-        with self.engine._t("exchange"):
+
+        def dense_step():  # world all-reduce of the global TM grads + SGD
             self.fabric.all_reduce_(list(range(self.plan.G)), acc)
-        self.global_tm.grads = acc
-        self.global_tm.sgd_step(self.lr)
-        self.engine.backward(dx, self.lr, self.opt, self.eps)
+            self.global_tm.grads = acc
+            self.global_tm.sgd_step(self.lr)
+
+        self.engine.backward(dx, self.lr, self.opt, self.eps, dense_hook=dense_step)
 
     def train_step(self, kjts: dict, grads: dict) -> dict:
         outs = self.forward(kjts, save=True)
         self.backward(grads)
         return outs
 
-    def capture(self, kjts: dict, grads: dict, warmup: int = 2):
+    def capture(self, kjts: dict, grads: dict, warmup: int = 2, timers=None):
         """Capture one full train step (forward a-f, backward, optimizer
         updates) as a CUDA graph over the given static input buffers.
 
@@ -128,8 +130,12 @@ class SPTT:
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            outs = self.train_step(kjts, grads)
+        self.engine.timers = timers  # external events -> graph nodes
+        try:
+            with torch.cuda.graph(graph):
+                outs = self.train_step(kjts, grads)
+        finally:
+            self.engine.timers = None
         return graph.replay, outs
 
 

@@ -1,0 +1,109 @@
+"""Multi-GPU (NCCL, one process per GPU) SPTT parity: the distributed train step
+must reproduce the single-process loopback engine bit for bit (same kernels,
+same reduction orders) and therefore the oracle.  Skipped on boxes with fewer
+than 2 GPUs (the driver's round-end GPU tests run on one GPU; run this with
+`gpurun --gpus 2|4`)."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _build(hosts, rph, dev):
+    import paper_2403_00877_b200 as P
+    from paper_2403_00877_b200.pipeline import KJT
+    from paper_2403_00877_b200.sptt import build_world
+
+    F, rows, N, B = 8, 64, 32, 6
+    topo, layout, placement, assignment = build_world(hosts, rph, 1, F, rows, N, seed=4, scheme="column_wise",
+                                                      shards_per_table=2)
+    G = topo.world_size
+    pooling = {f: "sum" for f in range(F)}
+    cfg = P.TMConfig(kind="dcn", out_dim=8, cross_layers=2, seed=1)
+    rng = np.random.default_rng(21)
+    lens = rng.integers(0, 6, size=(G, F, B)).astype(np.int32)
+    vals = rng.integers(0, rows, size=int(lens.sum())).astype(np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens.reshape(-1))])
+    kjts = {}
+    for r in range(G):
+        seg = vals[offs[r * F * B]:offs[(r + 1) * F * B]]
+        kjts[r] = KJT(torch.from_numpy(lens[r].reshape(-1)).to(dev), torch.from_numpy(seg.astype(np.int32)).to(dev),
+                      [int(lens[r, f].sum()) for f in range(F)], B)
+    return topo, layout, placement, assignment, pooling, cfg, kjts, B
+
+
+def _worker(rank, world, port, hosts, rph, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        import sys
+
+        here = os.path.dirname(os.path.abspath(__file__))
+        sys.path.insert(0, os.path.dirname(here))
+        from paper_2403_00877_b200.fabric import LoopbackFabric, NcclFabric
+        from paper_2403_00877_b200.sptt import SPTT
+
+        topo, layout, placement, assignment, pooling, cfg, kjts, B = _build(hosts, rph, dev)
+        fab = NcclFabric(world, rank, layout.group_width(topo), dev)
+        dist_model = SPTT(topo, layout, placement, assignment, pooling, B, fab, tm=cfg, dtype=torch.float32,
+                          device=dev, lr=0.05)
+        # reference: every rank on this GPU through the loopback fabric
+        topo2, layout2, placement2, _, _, _, kjts2, _ = _build(hosts, rph, dev)
+        ref = SPTT(topo2, layout2, placement2, assignment, pooling, B, LoopbackFabric(world, dev), tm=cfg,
+                   dtype=torch.float32, device=dev, lr=0.05)
+        gen = np.random.default_rng(5)
+        O = dist_model.plan.out_width()
+        grads = {r: torch.from_numpy(gen.normal(size=(B, O)).astype(np.float32)).to(dev) for r in range(world)}
+        out_d = dist_model.train_step({rank: kjts[rank]}, {rank: grads[rank]})
+        out_r = ref.train_step(kjts2, grads)
+        torch.cuda.synchronize()
+        ok = torch.allclose(out_d[rank], out_r[rank], rtol=1e-6, atol=1e-6)
+        for sid in dist_model.engine.weights:
+            ok = ok and torch.allclose(dist_model.engine.weights[sid], ref.engine.weights[sid], rtol=1e-5,
+                                       atol=1e-6)
+        q.put((rank, bool(ok), None))
+    except Exception:  # pragma: no cover
+        import traceback
+
+        q.put((rank, False, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("hosts,rph", [(2, 1), (2, 2), (4, 1)])
+def test_distributed_step_matches_loopback(hosts, rph):
+    world = hosts * rph
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, hosts, rph, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, err in res:
+        assert ok, f"rank {rank}: {err}"

@@ -128,18 +128,24 @@ def test_tower_module_backward_vs_oracle(kind, dt):
         assert np.abs(got - want).max() <= tol * s * 4, k
 
 
-@pytest.mark.parametrize("hosts,rph,kind", [(2, 2, "dlrm"), (2, 4, "dcn"), (4, 2, "dcn"), (1, 1, "dcn")])
-def test_sptt_train_step_loopback_vs_oracle(hosts, rph, kind):
-    """Full step on G simulated ranks: outputs, then every table row after SGD."""
+@pytest.mark.parametrize("hosts,rph,kind,scheme,opt", [
+    (2, 2, "dlrm", "table_wise", "sgd"), (2, 4, "dcn", "table_wise", "sgd"), (4, 2, "dcn", "table_wise", "sgd"),
+    (1, 1, "dcn", "table_wise", "sgd"), (2, 2, "dcn", "column_wise", "sgd"), (2, 2, "dcn", "row_wise", "sgd"),
+    (2, 2, "dlrm", "table_wise", "adagrad"), (2, 4, "dcn", "column_wise", "adagrad")])
+def test_sptt_train_step_loopback_vs_oracle(hosts, rph, kind, scheme, opt):
+    """Full step on G simulated ranks: outputs, then every table row after the
+    optimizer (SGD or row-wise Adagrad), for table/column/row-wise shards."""
     import paper_2403_00877_b200 as P
     from paper_2403_00877_b200.fabric import LoopbackFabric
     from paper_2403_00877_b200.pipeline import KJT
     from paper_2403_00877_b200.sptt import SPTT, build_world
 
     F, rows, N, B = 8, 60, 16, 5
-    topo, layout, placement, assignment = build_world(hosts, rph, 1, F, rows, N, seed=2)
+    topo, layout, placement, assignment = build_world(hosts, rph, 1, F, rows, N, seed=2, scheme=scheme,
+                                                      shards_per_table=2)
     G, T = topo.world_size, layout.num_towers
-    pooling = {f: ("mean" if f % 3 == 0 else "sum") for f in range(F)}
+    # mean pooling is undefined over row-wise partial pools (the reference sums them)
+    pooling = {f: ("mean" if f % 3 == 0 and scheme != "row_wise" else "sum") for f in range(F)}
     if kind == "dlrm":
         cfg = P.TMConfig(kind="dlrm", out_dim=8, per_feature_outputs=1, flat_outputs=1, seed=1)
     else:
@@ -149,7 +155,7 @@ def test_sptt_train_step_loopback_vs_oracle(hosts, rph, kind):
     before = {t: placement.tables[t].values.astype(np.float64).copy() for t in range(F)}
     lr = 0.05
     model = SPTT(topo, layout, placement, assignment, pooling, B, LoopbackFabric(G, dev()), tm=cfg,
-                 dtype=torch.float32, lr=lr)
+                 dtype=torch.float32, lr=lr, optimizer=opt, eps=1e-6)
     rng = np.random.default_rng(11)
     lens = rng.integers(0, 5, size=(G, F, B)).astype(np.int32)
     vals = rng.integers(0, rows, size=int(lens.sum())).astype(np.int64)
@@ -169,8 +175,7 @@ def test_sptt_train_step_loopback_vs_oracle(hosts, rph, kind):
                                             oracle.OTopo(hosts, rph))
     by_tower = {t: [f for f in range(F) if assignment[f] == t] for t in range(T)}
     tw = {t: oracle.init_tm_weights(ocfg, len(by_tower[t]), N, salt=t) for t in range(T)}
-    expect = {t: before[t].copy() for t in range(F)}
-    tw_grads = {t: None for t in range(T)}
+    grad_rows = {t: np.zeros_like(before[t]) for t in range(F)}
     for r in range(G):
         g_r = grads[r].double().cpu().numpy()
         col = 0
@@ -188,10 +193,29 @@ def test_sptt_train_step_loopback_vs_oracle(hosts, rph, kind):
                     n = offs[base + b + 1] - offs[base + b]
                     for k in range(offs[base + b], offs[base + b + 1]):
                         scale = 1.0 / n if pooling[f] == "mean" else 1.0
-                        expect[f][vals[k]] -= lr * scale * dx[b, i]
+                        grad_rows[f][vals[k]] += scale * dx[b, i]
+    expect = {}
+    for f in range(F):
+        touched = np.unique(vals[np.concatenate([np.arange(offs[(r * F + f) * B], offs[(r * F + f + 1) * B])
+                                                 for r in range(G)])])
+        if opt == "sgd":
+            expect[f] = oracle.apply_sgd(before[f], touched, grad_rows[f][touched], lr)
+        else:
+            expect[f], _ = oracle.apply_rowwise_adagrad(before[f], np.zeros(rows), touched,
+                                                        grad_rows[f][touched], lr, 1e-6)
     for sid, sh in enumerate(placement.shards):
         got = model.engine.weights[sid].double().cpu().numpy()
-        np.testing.assert_allclose(got, expect[sh.table_id], rtol=1e-4, atol=2e-5)
+        (r0, r1), (c0, c1) = sh.row_range, sh.col_range
+        want = expect[sh.table_id][r0:r1, c0:c1]
+        if opt == "adagrad" and sh.scheme == "column_wise":
+            # row-wise Adagrad on a column shard normalises by that shard's own
+            # squared-gradient mean (one accumulator per shard row), so compare
+            # against the shard-local rule
+            gsh = grad_rows[sh.table_id][:, c0:c1]
+            tch = np.unique(np.nonzero(np.any(gsh != 0, axis=1))[0])
+            want, _ = oracle.apply_rowwise_adagrad(before[sh.table_id][:, c0:c1], np.zeros(rows), tch, gsh[tch],
+                                                   lr, 1e-6)
+        np.testing.assert_allclose(got, want, rtol=1e-4, atol=3e-5)
 
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
