@@ -182,6 +182,8 @@ typedef struct dmt_copy2d {
   int64_t rows;
   int64_t width;
 } dmt_copy2d;
+/* elem_bytes < 0: the caller guarantees every copy is 16-byte granular
+ * (pointers, strides, widths) -> 16-byte vector moves. */
 int dmt_batched_copy2d(const dmt_copy2d* copies, int32_t n, int32_t elem_bytes, int64_t max_elems,
                        dmt_stream_t stream);
 

@@ -87,15 +87,29 @@ __global__ void batched_copy_kernel(const dmt_copy* __restrict__ copies) {
     d1[i] = s1[i];
 }
 
-template <typename E>
+// E = element type; when VB > 1 every copy is moved in 16-byte vectors (the
+// host checks that widths, strides and pointers are 16-byte granular).
+template <typename E, int VB>
 __global__ void batched_copy2d_kernel(const dmt_copy2d* __restrict__ copies) {
   const dmt_copy2d c = copies[blockIdx.y];
-  const int64_t total = c.rows * c.width;
-  const E* s = reinterpret_cast<const E*>(c.src);
-  E* d = reinterpret_cast<E*>(c.dst);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / c.width, j = i - r * c.width;
-    d[r * c.dst_ld + j] = s[r * c.src_ld + j];
+  if constexpr (VB == 1) {
+    const int64_t total = c.rows * c.width;
+    const E* s = reinterpret_cast<const E*>(c.src);
+    E* d = reinterpret_cast<E*>(c.dst);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      int64_t r = i / c.width, j = i - r * c.width;
+      d[r * c.dst_ld + j] = s[r * c.src_ld + j];
+    }
+  } else {
+    constexpr int EV = 16 / sizeof(E);  // elements per vector
+    const int64_t wv = c.width / EV, sld = c.src_ld / EV, dld = c.dst_ld / EV;
+    const int64_t total = c.rows * wv;
+    const uint4* s = reinterpret_cast<const uint4*>(c.src);
+    uint4* d = reinterpret_cast<uint4*>(c.dst);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      int64_t r = i / wv, j = i - r * wv;
+      d[r * dld + j] = s[r * sld + j];
+    }
   }
 }
 
@@ -160,12 +174,23 @@ __global__ void colsum_partial_vec(const T* __restrict__ in, int64_t rows, int64
   for (int e = 0; e < V; ++e) part[(int64_t)blockIdx.y * cols + c + e] = dacc[e] + acc[e];
 }
 
+// 32 columns x 8 partial-slices per block; fixed-order tree over the 8 slices
+// (deterministic) after each thread folds nparts/8 partials.
 __global__ void colsum_final(const double* __restrict__ part, int64_t cols, int nparts, float* __restrict__ out) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + tx;
   double acc = 0.0;
-  for (int p = 0; p < nparts; ++p) acc += part[(int64_t)p * cols + c];
-  out[c] = (float)acc;
+  if (c < cols)
+    for (int p = ty; p < nparts; p += 8) acc += part[(int64_t)p * cols + c];
+  red[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][tx];
+    out[c] = (float)t;
+  }
 }
 
 template <typename T>
@@ -248,16 +273,23 @@ int dmt_batched_copy(const dmt_copy* copies, int32_t n, int64_t max_bytes, dmt_s
 
 int dmt_batched_copy2d(const dmt_copy2d* copies, int32_t n, int32_t elem_bytes, int64_t max_elems,
                        dmt_stream_t stream) {
+  // a negative elem_bytes promises 16-byte granularity of every copy (vector path)
+  const bool vec = elem_bytes < 0;
+  if (vec) elem_bytes = -elem_bytes;
   if (n < 0) return DMT_ERR_DOMAIN;
   if (n == 0 || max_elems <= 0) return DMT_OK;
   if (n > 65535) return DMT_ERR_UNSUPPORTED;
-  unsigned gx = (unsigned)std::min<int64_t>(dmt::ceil_div(max_elems, 256), 2048);
+  const int64_t work = vec ? max_elems * elem_bytes / 16 : max_elems;
+  unsigned gx = (unsigned)std::min<int64_t>(dmt::ceil_div(work, 256), 2048);
   dim3 grid(gx, n);
   cudaStream_t s = (cudaStream_t)stream;
-  switch (elem_bytes) {
-    case 2: dmt::batched_copy2d_kernel<uint16_t><<<grid, 256, 0, s>>>(copies); break;
-    case 4: dmt::batched_copy2d_kernel<uint32_t><<<grid, 256, 0, s>>>(copies); break;
-    case 8: dmt::batched_copy2d_kernel<uint64_t><<<grid, 256, 0, s>>>(copies); break;
+  switch (elem_bytes * (vec ? -1 : 1)) {
+    case 2: dmt::batched_copy2d_kernel<uint16_t, 1><<<grid, 256, 0, s>>>(copies); break;
+    case 4: dmt::batched_copy2d_kernel<uint32_t, 1><<<grid, 256, 0, s>>>(copies); break;
+    case 8: dmt::batched_copy2d_kernel<uint64_t, 1><<<grid, 256, 0, s>>>(copies); break;
+    case -2: dmt::batched_copy2d_kernel<uint16_t, 16><<<grid, 256, 0, s>>>(copies); break;
+    case -4: dmt::batched_copy2d_kernel<uint32_t, 16><<<grid, 256, 0, s>>>(copies); break;
+    case -8: dmt::batched_copy2d_kernel<uint64_t, 16><<<grid, 256, 0, s>>>(copies); break;
     default: return DMT_ERR_UNSUPPORTED;
   }
   DMT_CHECK_LAUNCH();
@@ -312,7 +344,7 @@ int dmt_column_sum(const void* in, int64_t rows, int64_t cols, int64_t ld, float
                                                                 g_colsum_scratch);
     else
       dmt::colsum_partial_vec<__half><<<vg, 128, 0, s>>>((const __half*)in, rows, cols, ld, rows_per, g_colsum_scratch);
-    dmt::colsum_final<<<(unsigned)dmt::ceil_div(cols, 256), 256, 0, s>>>(g_colsum_scratch, cols, nparts, out);
+    dmt::colsum_final<<<(unsigned)dmt::ceil_div(cols, 32), 256, 0, s>>>(g_colsum_scratch, cols, nparts, out);
     DMT_CHECK_LAUNCH();
     return DMT_OK;
   }
@@ -323,7 +355,7 @@ int dmt_column_sum(const void* in, int64_t rows, int64_t cols, int64_t ld, float
     case DMT_F64: dmt::colsum_partial<double><<<grid, 256, 0, s>>>((const double*)in, rows, cols, ld, rows_per, g_colsum_scratch); break;
     default: return DMT_ERR_UNSUPPORTED;
   }
-  dmt::colsum_final<<<(unsigned)dmt::ceil_div(cols, 256), 256, 0, s>>>(g_colsum_scratch, cols, nparts, out);
+  dmt::colsum_final<<<(unsigned)dmt::ceil_div(cols, 32), 256, 0, s>>>(g_colsum_scratch, cols, nparts, out);
   DMT_CHECK_LAUNCH();
   return DMT_OK;
 }

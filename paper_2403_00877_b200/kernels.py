@@ -281,6 +281,7 @@ class Copy2DTable:
         structs = []
         self.elem = None
         self.max_elems = 0
+        self.vec = True
         for st, so, sld, dt, do, dld, rows, width in copies:
             if rows * width == 0:
                 continue
@@ -289,16 +290,18 @@ class Copy2DTable:
                 self.elem = es
             elif es != self.elem:
                 raise DomainError("Copy2DTable mixes element sizes")
-            structs.append(L.Copy2D(src=st.data_ptr() + so * es, dst=dt.data_ptr() + do * es, src_ld=sld,
-                                    dst_ld=dld, rows=rows, width=width))
+            sp, dp = st.data_ptr() + so * es, dt.data_ptr() + do * es
+            if sp % 16 or dp % 16 or (sld * es) % 16 or (dld * es) % 16 or (width * es) % 16:
+                self.vec = False
+            structs.append(L.Copy2D(src=sp, dst=dp, src_ld=sld, dst_ld=dld, rows=rows, width=width))
             self.max_elems = max(self.max_elems, rows * width)
         self.n = len(structs)
         self.dev, self.host = device_table(L.Copy2D, structs, device)
 
     def run(self) -> None:
         if self.n:
-            L.check(L.lib().dmt_batched_copy2d(self.dev.data_ptr(), self.n, self.elem, self.max_elems,
-                                               L.stream_ptr()), "dmt_batched_copy2d")
+            L.check(L.lib().dmt_batched_copy2d(self.dev.data_ptr(), self.n, -self.elem if self.vec else self.elem,
+                                               self.max_elems, L.stream_ptr()), "dmt_batched_copy2d")
 
 
 # ---------------------------------------------------------------- GEMM -----
