@@ -284,6 +284,9 @@ int dmt_convert(const void* src, int32_t dtype_in, void* dst, int32_t dtype_out,
 /* Library identification: returns a static string ("libdmt <version> sm_100a"). */
 const char* dmt_version(void);
 
+/* Text of the last CUDA error behind a DMT_ERR_CUDA status (this thread). */
+const char* dmt_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

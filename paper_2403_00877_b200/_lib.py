@@ -66,6 +66,7 @@ class GemmArgs(C.Structure):
 
 _SIGS = {
     "dmt_version": (C.c_char_p, []),
+    "dmt_last_error": (C.c_char_p, []),
     "dmt_lengths_to_offsets_workspace_size": (sz, [i64]),
     "dmt_lengths_to_offsets": (C.c_int, [vp, i64, vp, vp, vp]),
     "dmt_kjt_bucketize": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]),
@@ -125,7 +126,10 @@ def check(status: int, what: str) -> None:
     CALLS[0] += 1
     if status != 0:
         cls = STATUS_ERRORS.get(status, TowersimError)
-        raise cls(f"{what} failed with libdmt status {status}")
+        extra = ""
+        if status == -10:
+            extra = ": " + _lib.dmt_last_error().decode()
+        raise cls(f"{what} failed with libdmt status {status}{extra}")
 
 
 def stream_ptr(stream=None) -> int:

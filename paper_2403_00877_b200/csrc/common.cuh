@@ -10,10 +10,17 @@
 
 #define DMT_NUM_SMS 148
 
+namespace dmt {
+void set_last_error(cudaError_t e);
+}
+
 #define DMT_CHECK_LAUNCH()                          \
   do {                                              \
     cudaError_t e_ = cudaGetLastError();            \
-    if (e_ != cudaSuccess) return DMT_ERR_CUDA;     \
+    if (e_ != cudaSuccess) {                        \
+      dmt::set_last_error(e_);                      \
+      return DMT_ERR_CUDA;                          \
+    }                                               \
   } while (0)
 
 namespace dmt {

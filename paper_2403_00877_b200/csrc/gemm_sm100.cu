@@ -530,6 +530,61 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       const uint32_t acc_phase = (it >> 1) & 1;
       const int64_t m0 = (tile / tiles_n) * kBlockM;
       const int64_t n0 = (tile % tiles_n) * BN;
+      float* stile = stile_all + (warp - 2) * kStileFloats;
+      if (p.coalesced && n0 + (int64_t)(half + 1) * kColsPerWarp <= p.n) {
+        // Pipelined full-width path: the epilogue operands (x0 / u / C / dx0)
+        // do not depend on the accumulator, so the loads of slab-pair k+1 are
+        // issued before slab-pair k is finished -- and the first ones before
+        // the accumulator barrier -- hiding their latency behind the MMAs.
+        // slab k = 8 rows x 32 columns of this warp's chunk (k & 3) of chunk k >> 2
+        constexpr int kSlabs = (kColsPerWarp / 32) * 4;
+        const int c8 = (lane & 3) * 8;
+        auto slab_pos = [&](int k, int64_t& r, int64_t& col) {
+          col = n0 + half * kColsPerWarp + (k >> 2) * 32 + c8;
+          r = m0 + q * 32 + (k & 3) * 8 + (lane >> 2);
+        };
+        EpiIn<TIN, TO> nx;
+        {
+          int64_t r, col;
+          slab_pos(0, r, col);
+          if (r < p.m) epi_load<TIN, TO>(p, r, col, nx);
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int k = 0; k < kSlabs; ++k) {
+          if ((k & 3) == 0) {  // stage the next 32-column chunk of the accumulator
+            float v[32];
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) +
+                          (uint32_t)(acc * BN + half * kColsPerWarp + (k >> 2) * 32), v);
+            if (p.scale_acc) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) stile[lane * 33 + i] = v[i];
+            __syncwarp();
+          }
+          EpiIn<TIN, TO> cur = nx;
+          int64_t r, col;
+          slab_pos(k, r, col);
+          if (k + 1 < kSlabs) {
+            int64_t rn, coln;
+            slab_pos(k + 1, rn, coln);
+            if (rn < p.m) epi_load<TIN, TO>(p, rn, coln, nx);
+          }
+          const int rl = (k & 3) * 8 + (lane >> 2);
+          float a[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) a[j] = stile[rl * 33 + c8 + j];
+          if (r < p.m) epi_finish<TIN, TO>(p, r, col, a, cur);
+        }
+        __syncwarp();
+        tc_fence_before();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        continue;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t row = m0 + q * 32 + lane;
@@ -537,7 +592,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       TO* drow = nullptr;
       if (row_ok)
         drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
-      float* stile = stile_all + (warp - 2) * kStileFloats;
 #pragma unroll 1
       for (int c = half * kColsPerWarp; c < (half + 1) * kColsPerWarp; c += 32) {
         float v[32];
@@ -760,8 +814,11 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   auto kern = gemm_kernel<BN, NOPS, KIND, STAGES, TIN, TO, AMN, BMN>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    if (e != cudaSuccess) {
+      set_last_error(e);
       return DMT_ERR_CUDA;
+    }
     attr_set = true;
   }
   int64_t tiles = ceil_div(a->m, kBlockM) * ceil_div(a->n, BN);

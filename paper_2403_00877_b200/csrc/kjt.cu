@@ -5,6 +5,8 @@
 // (towersim/exchange.py:162-178).  On the device that is a jagged gather of
 // per-feature (lengths, values) segments into per-owner send slots; the
 // all-to-all that follows is NCCL (or an in-process copy) on these buffers.
+#include <cstdio>
+
 #include "common.cuh"
 
 namespace dmt {
@@ -184,5 +186,19 @@ int dmt_kjt_slot_offsets(const int64_t* offsets, int32_t B, int32_t num_slots, c
 }
 
 const char* dmt_version(void) { return "libdmt 0.1.0 sm_100a"; }
+
+static thread_local char g_last_error[256] = "no error";
+
+const char* dmt_last_error(void) { return g_last_error; }
+
+}  // extern "C"
+
+namespace dmt {
+void set_last_error(cudaError_t e) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s (%d)", cudaGetErrorString(e), (int)e);
+}
+}  // namespace dmt
+
+extern "C" {
 
 }  // extern "C"
