@@ -11,6 +11,8 @@
 // reference's sequential sum.  Each segment's output pointer/stride encodes the
 // destination layout, which is how the step-c permute and step-d stacking are
 // fused into the lookup epilogue (zero extra bytes).
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -84,10 +86,10 @@ struct Frag {
 };
 
 constexpr int kLookupThreads = 256;
-constexpr int kUnroll = 8;
+constexpr int kUnroll = 8;  // default rows in flight per thread (see UN below)
 
 // G threads per bag (power of two <= 32), NV vectors of VEC elements per thread.
-template <typename T, int VEC, int NV>
+template <typename T, int VEC, int NV, int UN = kUnroll>
 __global__ void __launch_bounds__(kLookupThreads)
 pooled_fwd_kernel(const dmt_lookup_segment* __restrict__ segs, const int64_t* __restrict__ offsets,
                   const int32_t* __restrict__ indices, int log2g, int32_t* __restrict__ err) {
@@ -126,11 +128,11 @@ pooled_fwd_kernel(const dmt_lookup_segment* __restrict__ segs, const int64_t* __
   if (sg.pooling == DMT_POOL_NONE && len != 1 && err) atomicOr(err, DMT_EBIT_BAGLEN);
 
   int bad = 0;
-  for (int64_t k0 = beg; k0 < end; k0 += kUnroll) {
-    Frag<T, VEC> fr[kUnroll][NV];
-    bool use[kUnroll];
+  for (int64_t k0 = beg; k0 < end; k0 += UN) {
+    Frag<T, VEC> fr[UN][NV];
+    bool use[UN];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < UN; ++u) {
       use[u] = false;
       if (k0 + u < end) {
         int64_t r = (int64_t)__ldg(indices + k0 + u) - row_begin;
@@ -147,7 +149,7 @@ pooled_fwd_kernel(const dmt_lookup_segment* __restrict__ segs, const int64_t* __
     }
     // fold strictly in bag order (bit-exact sequential sum)
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
+    for (int u = 0; u < UN; ++u)
       if (use[u])
 #pragma unroll
         for (int v = 0; v < NV; ++v) fr[u][v].add_to(acc[v]);
@@ -223,7 +225,17 @@ int launch_fwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     int NV = (nvec + G - 1) / G;
     int bags_per_block = kLookupThreads / G;
     dim3 grid((unsigned)ceil_div(max_b, bags_per_block), n);
-    if (NV == 1)
+    static int un = [] {
+      const char* e = getenv("DMT_LOOKUP_UNROLL");  // tuning knob (default 8)
+      return e ? atoi(e) : 8;
+    }();
+    if (NV == 1 && un == 4)
+      pooled_fwd_kernel<T, VEC, 1, 4><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
+    else if (NV == 1 && un == 6)
+      pooled_fwd_kernel<T, VEC, 1, 6><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
+    else if (NV == 1 && un == 12)
+      pooled_fwd_kernel<T, VEC, 1, 12><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
+    else if (NV == 1)
       pooled_fwd_kernel<T, VEC, 1><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
     else if (NV == 2)
       pooled_fwd_kernel<T, VEC, 2><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
