@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--cross-layers", type=int, default=3)
     ap.add_argument("--towers", type=int, default=0, help="0 = auto (1 at N=1, else 2)")
     ap.add_argument("--no-flat", action="store_true", help="skip the flat-baseline comparison at N>1")
+    ap.add_argument("--fabric", default="peer", choices=["peer", "nccl"],
+                    help="N>1 SPTT exchange: NVLink peer stores + barrier (peer) or NCCL all-to-alls")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling runs)")
     ap.add_argument("--cpu-sample", type=int, default=256, help="samples per CPU-baseline step")
@@ -194,6 +196,8 @@ def _config(args, N):
             "batch_per_gpu": args.batch, "global_batch": args.batch * N, "tm": args.tm, "tm_out_dim": args.tm_out,
             "cross_layers": args.cross_layers, "towers": T, "gpus_per_tower": N // T, "optimizer": "sgd",
             "parallelism": f"embedding model-parallel in tower, TM data-parallel in tower (T={T}, W={N // T})",
+            "exchange": "loopback" if N == 1 else ("nvlink peer stores + barrier" if args.fabric == "peer"
+                                                   else "nccl all-to-all"),
             "l2": "inputs larger than L2 (tables >= 6.6 GB bf16, uniform random rows), no flush"}
 
 
@@ -216,7 +220,7 @@ def main():
 
     import paper_2403_00877_b200 as P
     from paper_2403_00877_b200 import _lib
-    from paper_2403_00877_b200.fabric import LoopbackFabric, NcclFabric
+    from paper_2403_00877_b200.fabric import LoopbackFabric, NcclFabric, PeerFabric
     from paper_2403_00877_b200.pipeline import KJT, PhaseTimers
     from paper_2403_00877_b200.sptt import SPTT, device_world, random_kjt
 
@@ -240,10 +244,12 @@ def main():
     topo, layout, placement, assignment = device_world(*topo_args, F, args.rows, Nd, dtype, [rank], seed=0, device=dev)
     pooling = {f: "sum" for f in range(F)}
 
-    def make_fabric():
-        return NcclFabric(N, rank, W, dev) if world > 1 else LoopbackFabric(1, dev)
+    def make_fabric(kind="nccl"):
+        if world == 1:
+            return LoopbackFabric(1, dev)
+        return (PeerFabric if kind == "peer" else NcclFabric)(N, rank, W, dev)
 
-    fabric = make_fabric()
+    fabric = make_fabric(args.fabric)
     tm_cfg = None if args.tm == "passthrough" else P.TMConfig(kind=args.tm, out_dim=args.tm_out, cross_layers=args.cross_layers,
                                                              per_feature_outputs=1, flat_outputs=0, seed=0)
     model = SPTT(topo, layout, placement, assignment, pooling, B, fabric, tm=tm_cfg, dtype=dtype, device=dev,

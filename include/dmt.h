@@ -284,6 +284,20 @@ int dmt_convert(const void* src, int32_t dtype_in, void* dst, int32_t dtype_out,
 /* Library identification: returns a static string ("libdmt <version> sm_100a"). */
 const char* dmt_version(void);
 
+/* Enable NVLink peer access from the current device to `peer_device` (needed
+ * before kernels store into another GPU's IPC-mapped exchange buffers). */
+int dmt_enable_peer_access(int peer_device);
+
+/* CUDA IPC for the NVLink peer exchange.  dmt_ipc_export writes the 64-byte
+ * handle of the allocation holding `ptr` and ptr's byte offset inside it;
+ * dmt_ipc_open maps a peer's handle into the CURRENT device's context (peer
+ * access enabled lazily) and returns the allocation base; dmt_ipc_close
+ * unmaps it.  Replaces nothing in the reference (its fabric is simulated,
+ * towersim/simnet.py); it is the B200 transport under step d / step f. */
+int dmt_ipc_export(const void* ptr, void* handle64, int64_t* offset);
+int dmt_ipc_open(const void* handle64, void** base);
+int dmt_ipc_close(void* base);
+
 /* Text of the last CUDA error behind a DMT_ERR_CUDA status (this thread). */
 const char* dmt_last_error(void);
 

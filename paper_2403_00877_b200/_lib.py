@@ -67,6 +67,10 @@ class GemmArgs(C.Structure):
 _SIGS = {
     "dmt_version": (C.c_char_p, []),
     "dmt_last_error": (C.c_char_p, []),
+    "dmt_enable_peer_access": (C.c_int, [C.c_int]),
+    "dmt_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    "dmt_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "dmt_ipc_close": (C.c_int, [C.c_void_p]),
     "dmt_lengths_to_offsets_workspace_size": (sz, [i64]),
     "dmt_lengths_to_offsets": (C.c_int, [vp, i64, vp, vp, vp]),
     "dmt_kjt_bucketize": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]),

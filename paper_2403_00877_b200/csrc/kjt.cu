@@ -5,7 +5,10 @@
 // (towersim/exchange.py:162-178).  On the device that is a jagged gather of
 // per-feature (lengths, values) segments into per-owner send slots; the
 // all-to-all that follows is NCCL (or an in-process copy) on these buffers.
+#include <dlfcn.h>
+
 #include <cstdio>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -186,6 +189,80 @@ int dmt_kjt_slot_offsets(const int64_t* offsets, int32_t B, int32_t num_slots, c
 }
 
 const char* dmt_version(void) { return "libdmt 0.1.0 sm_100a"; }
+
+int dmt_enable_peer_access(int peer_device) {
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) return DMT_ERR_CUDA;
+  if (peer_device == cur) return DMT_OK;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, cur, peer_device) != cudaSuccess || !can) return DMT_ERR_UNSUPPORTED;
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky-free status
+    return DMT_OK;
+  }
+  if (e != cudaSuccess) {
+    dmt::set_last_error(e);
+    return DMT_ERR_CUDA;
+  }
+  return DMT_OK;
+}
+
+// Allocation base of a device pointer through the driver API, resolved at run
+// time so the library does not link libcuda (CPU-only hosts load it too).
+static int alloc_base(const void* ptr, uintptr_t* base) {
+  typedef int (*range_fn)(unsigned long long*, size_t*, unsigned long long);
+  static range_fn fn = nullptr;
+  if (!fn) {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+    if (!h) return DMT_ERR_UNSUPPORTED;
+    fn = (range_fn)dlsym(h, "cuMemGetAddressRange_v2");
+    if (!fn) return DMT_ERR_UNSUPPORTED;
+  }
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (unsigned long long)(uintptr_t)ptr) != 0) return DMT_ERR_DOMAIN;
+  *base = (uintptr_t)b;
+  return DMT_OK;
+}
+
+int dmt_ipc_export(const void* ptr, void* handle64, int64_t* offset) {
+  if (!ptr || !handle64 || !offset) return DMT_ERR_DOMAIN;
+  uintptr_t base = 0;
+  int st = alloc_base(ptr, &base);
+  if (st != DMT_OK) return st;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, (void*)base);
+  if (e != cudaSuccess) {
+    dmt::set_last_error(e);
+    return DMT_ERR_CUDA;
+  }
+  memcpy(handle64, &h, sizeof(h));
+  *offset = (int64_t)((uintptr_t)ptr - base);
+  return DMT_OK;
+}
+
+int dmt_ipc_open(const void* handle64, void** base) {
+  if (!handle64 || !base) return DMT_ERR_DOMAIN;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    dmt::set_last_error(e);
+    return DMT_ERR_CUDA;
+  }
+  return DMT_OK;
+}
+
+int dmt_ipc_close(void* base) {
+  cudaError_t e = cudaIpcCloseMemHandle(base);
+  if (e != cudaSuccess) {
+    dmt::set_last_error(e);
+    return DMT_ERR_CUDA;
+  }
+  return DMT_OK;
+}
 
 static thread_local char g_last_error[256] = "no error";
 

@@ -144,3 +144,86 @@ class NcclFabric(Fabric):
         pg = self._pg(group)
         for t in tensors.values():
             self.dist.all_reduce(t, group=pg)
+
+
+class PeerBuffer:
+    """A peer rank's exchange buffer mapped into this process: enough of the
+    tensor interface (data_ptr / element_size / dtype / numel) for descriptor
+    tables, which is all the producing kernels need."""
+
+    def __init__(self, ptr: int, dtype, numel: int, rank: int):
+        self.ptr, self.dtype, self._numel, self.rank = ptr, dtype, numel, rank
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def element_size(self) -> int:
+        return torch.empty((), dtype=self.dtype).element_size()
+
+    def numel(self) -> int:
+        return self._numel
+
+
+class PeerFabric(NcclFabric):
+    """NCCL plumbing plus NVLink peer memory: receive buffers of every rank are
+    mapped into every other rank's address space (CUDA IPC through
+    torch.multiprocessing's CUDA-tensor sharing), so producing kernels can
+    write their exchange blocks straight into the consumer GPU's buffer.  A
+    collective step then reduces to one tiny stream-ordered NCCL all-reduce per
+    group used as a completion barrier (capturable in CUDA graphs)."""
+
+    p2p = True
+
+    def __init__(self, world_size: int, rank: int, W: int, backend_device=None):
+        super().__init__(world_size, rank, W, backend_device)
+        self._flag = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self._opened: dict = {}
+
+    def share(self, tensors: dict) -> dict:
+        """Collective over the world: every rank contributes {name: tensor};
+        returns {rank: {name: buffer}} where a peer's buffer is a PeerBuffer
+        mapped into THIS device's context (CUDA IPC opened under the accessing
+        device, peer access enabled lazily -- the NVLink P2P transport) and the
+        own rank's entries are the original tensors."""
+        import ctypes as C
+
+        from . import _lib as L
+
+        lib = L.lib()
+        mine = {}
+        for k, v in tensors.items():
+            h = (C.c_char * 64)()
+            off = C.c_int64()
+            L.check(lib.dmt_ipc_export(C.c_void_p(v.data_ptr()), h, C.byref(off)), "dmt_ipc_export")
+            mine[k] = (bytes(h), off.value, v.dtype, v.numel())
+        allv = [None] * self.world_size
+        self.dist.all_gather_object(allv, mine)
+        out = {}
+        for r, objs in enumerate(allv):
+            if r == self.rank:
+                out[r] = dict(tensors)
+                continue
+            mapped = {}
+            for k, (h, off, dtype, numel) in objs.items():
+                base = self._opened.get((r, h))
+                if base is None:
+                    p = C.c_void_p()
+                    L.check(lib.dmt_ipc_open(C.create_string_buffer(h, 64), C.byref(p)), "dmt_ipc_open")
+                    base = self._opened[(r, h)] = p.value
+                mapped[k] = PeerBuffer(base + off, dtype, numel, r)
+            out[r] = mapped
+        return out
+
+    def close(self) -> None:
+        from . import _lib as L
+
+        for base in self._opened.values():
+            L.lib().dmt_ipc_close(base)
+        self._opened.clear()
+
+    def barrier_(self, group) -> None:
+        """Completion barrier for peer writes: every member's preceding kernels
+        (stream order) finished before any member passes it."""
+        if len(group) == 1:
+            return
+        self.dist.all_reduce(self._flag, group=self._pg(group))

@@ -167,6 +167,60 @@ class SpttEngine:
         self.uniform_nnz = False
         self._side = None
         self._prepared: dict = {}
+        self.p2p_d = self.p2p_f = False
+        if getattr(fabric, "p2p", False) and sptt:
+            self._init_peer_links()
+
+    # ------------------------------------------------------- NVLink peers ----
+    def _init_peer_links(self) -> None:
+        """Map every rank's exchange buffers (PeerFabric.share) and build the
+        descriptor tables whose destinations are *peer* addresses: the pooled
+        lookup writes its step-d blocks straight into the tower members'
+        receive buffers (step c + d fused into the gather), and step f, f^-1
+        and d^-1 become one peer-store launch each.  One rank per process."""
+        p, dev = self.plan, self.device
+        (r,) = self.local
+        b = self.buf[r]
+        self.p2p_d = p.W > 1
+        self.p2p_f = p.T > 1
+        share = {"recv_d": b["recv_d"], "recv_f": b["recv_f"], "grad_x": b["grad_x"]}
+        if self.p2p_f:
+            share["g_y"] = self._persist(r, "g_y", b["Y"])
+        self.peer = self.fabric.share(share)
+        if self.p2p_d:
+            segs = []
+            for seg, (pp, k, off, w) in zip(self.seg_fwd[r].segments, p.lookup_out_offsets(r, True)):
+                c, j = pp % p.W, pp // p.W
+                m = p.tower_of(r) * p.W + c
+                dst = self.peer[m]["recv_d"]
+                segs.append(K.Segment(weights=seg.weights, out=dst, out_offset=p.d_recv_offset(m, r, k) + j * p.B * w,
+                                      out_ld=w, bag_begin=seg.bag_begin, nbags=seg.nbags, pooling=seg.pooling,
+                                      row_begin=seg.row_begin, row_filter=seg.row_filter, key_base=seg.key_base))
+            self.seg_fwd_p2p = K.SegmentTable(segs, dev)
+
+    def _f_peer_copies(self, r: int) -> K.CopyTable:
+        """Step f: Y block j -> the class member in tower j (its recv_f slot)."""
+        p = self.plan
+        t, c = p.tower_of(r), r % p.W
+        Y = self.buf[r]["Y"]
+        es = Y.element_size()
+        blk = p.B * p.O[t]
+        off_recv = p.B * sum(p.O[t2] for t2 in range(t))
+        copies = []
+        for j in range(p.T):
+            dst = self.peer[j * p.W + c]["recv_f"]
+            copies.append((Y.data_ptr() + j * blk * es, dst.data_ptr() + off_recv * es, blk * es))
+        return K.CopyTable(copies, self.device)
+
+    def _record_d(self, r: int) -> None:
+        if self.trace is not None:
+            for m in self.plan.group_of(r):
+                self.trace.record_elements("d", r, m, self.plan.d_send_splits(r)[0], self.es)
+
+    def _record_f(self, r: int) -> None:
+        if self.trace is not None:
+            for m in self.plan.class_group_of(r):
+                self.trace.record_elements("f", r, m, self.plan.f_send_splits(r)[0], self.es)
 
     def _t(self, name: str):
         return _Scope(self.timers, name)
@@ -270,7 +324,8 @@ class SpttEngine:
         for r in self.local:
             offsets = K.lengths_to_offsets(recv_len[r][: p.owner_bags(r)])
             with self._t("lookup_fwd"):
-                K.pooled_lookup_fwd(self.seg_fwd[r], offsets, recv_val[r], err)
+                table = self.seg_fwd_p2p if self.p2p_d else self.seg_fwd[r]
+                K.pooled_lookup_fwd(table, offsets, recv_val[r], err)
             nnz = sum(recv_val_splits[r])
             self._owner[r] = (offsets, recv_val[r], nnz)
             if save:
@@ -287,10 +342,16 @@ class SpttEngine:
             K.raise_lookup_errors(err)
         if self.mode == "flat":
             return self._flat_forward()
-        # step d: tower all-to-alls
+        # step d: tower all-to-alls (or, over NVLink peers, the lookup already
+        # stored every block in its member's receive buffer: barrier only)
         send = {r: self.buf[r]["send_x"] for r in self.local}
         recv = {r: self.buf[r]["recv_d"] for r in self.local}
         for g in self._groups(p.group_of):
+            if self.p2p_d:
+                self._record_d(self.local[0])
+                with self._t("exchange_d"):
+                    fab.barrier_(g)
+                continue
             self._trace_d(g)
             with self._t("exchange_d"):
                 fab.alltoallv(g, "d", send, {r: p.d_send_splits(r) for r in g}, recv,
@@ -308,6 +369,15 @@ class SpttEngine:
         send = {r: self.buf[r]["Y"].view(-1) for r in self.local}
         recv = {r: self.buf[r]["recv_f"] for r in self.local}
         for g in self._groups(p.class_group_of):
+            if self.p2p_f:
+                (r,) = self.local
+                self._record_f(r)
+                with self._t("exchange_f"):
+                    if "f_copies" not in self.buf[r]:
+                        self.buf[r]["f_copies"] = self._f_peer_copies(r)
+                    self.buf[r]["f_copies"].run()  # peer stores over NVLink
+                    fab.barrier_(g)
+                continue
             with self._t("exchange_f"):
                 fab.alltoallv(g, "f", send, {r: p.f_send_splits(r) for r in g}, recv,
                               {r: p.f_recv_splits(r) for r in g}, self.trace, self.es)
@@ -381,6 +451,20 @@ class SpttEngine:
         # receive layout), send each block back to the member that produced it
         gsend, grecv = {}, {}
         for r in self.local:
+            if self.p2p_f:
+                # f^-1 over NVLink: the tower-t column block goes straight into
+                # the tower-t class member's g_y rows of this rank's tower
+                t_r, c = p.tower_of(r), r % p.W
+                copies, col, ow = [], 0, p.out_width()
+                for t in range(p.T):
+                    dst = self.peer[t * p.W + c]["g_y"]
+                    copies.append((grad_out[r], col, ow, dst, t_r * p.B * p.O[t], p.O[t], p.B, p.O[t]))
+                    col += p.O[t]
+                with self._t("exchange_f_bwd"):
+                    K.Copy2DTable(copies, dev).run()
+                    fab.barrier_(p.class_group_of(r))
+                grecv[r] = self.buf[r]["g_y"]
+                continue
             gf = self._persist(r, "g_f", self.buf[r]["recv_f"])
             copies = []
             col, off = 0, 0
@@ -393,7 +477,7 @@ class SpttEngine:
             gsend[r] = gf
             grecv[r] = (gf.view(p.T * p.B, p.O[p.tower_of(r)]) if p.T == 1 else
                         self._persist(r, "g_y", self.buf[r]["Y"]))
-        for g in self._groups(p.class_group_of):
+        for g in ([] if self.p2p_f else self._groups(p.class_group_of)):
             with self._t("exchange_f_bwd"):
                 fab.alltoallv(g, "f_bwd", gsend, {r: p.f_recv_splits(r) for r in g}, {r: grecv[r].view(-1) for r in self.local},
                               {r: p.f_send_splits(r) for r in g})
@@ -417,6 +501,22 @@ class SpttEngine:
         # d^-1: scatter dX columns back into the step-d receive layout
         dsend, drecv = {}, {}
         for r in self.local:
+            if self.p2p_d:
+                # d^-1 over NVLink: scatter dX columns straight into every
+                # owner's gradient buffer (its step-d send layout, member block c)
+                c = r % p.W
+                copies, xw = [], p.x_width(r)
+                for fb in p.e_blocks(r):
+                    for pc in fb.pieces:
+                        o = self.placement.shards[pc.sid].rank
+                        k = p.k_of(pc.sid)
+                        dst = self.peer[o]["grad_x"]
+                        off = c * p.T * p.B * p.SW[o] + p.T * p.B * p.pre[o][k]
+                        copies.append((dX[r], fb.dst_col + pc.c0, xw, dst, off, pc.ld, p.T * p.B, pc.width))
+                with self._t("exchange_d_bwd"):
+                    K.Copy2DTable(copies, dev).run()
+                    fab.barrier_(p.group_of(r))
+                continue
             gd = self.buf[r]["grad_x"] if p.W == 1 else self._persist(r, "g_d", self.buf[r]["recv_d"])
             copies = []
             xw = p.x_width(r)
@@ -426,7 +526,7 @@ class SpttEngine:
             K.Copy2DTable(copies, dev).run()
             dsend[r] = gd
             drecv[r] = self.buf[r]["grad_x"]
-        for g in self._groups(p.group_of):
+        for g in ([] if self.p2p_d else self._groups(p.group_of)):
             with self._t("exchange_d_bwd"):
                 fab.alltoallv(g, "d_bwd", dsend, {r: p.d_recv_splits(r) for r in g}, drecv,
                               {r: p.d_send_splits(r) for r in g})

@@ -47,7 +47,7 @@ def _build(hosts, rph, dev):
     return topo, layout, placement, assignment, pooling, cfg, kjts, B
 
 
-def _worker(rank, world, port, hosts, rph, q):
+def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
 
@@ -59,11 +59,12 @@ def _worker(rank, world, port, hosts, rph, q):
 
         here = os.path.dirname(os.path.abspath(__file__))
         sys.path.insert(0, os.path.dirname(here))
-        from paper_2403_00877_b200.fabric import LoopbackFabric, NcclFabric
+        from paper_2403_00877_b200.fabric import LoopbackFabric, NcclFabric, PeerFabric
         from paper_2403_00877_b200.sptt import SPTT
 
         topo, layout, placement, assignment, pooling, cfg, kjts, B = _build(hosts, rph, dev)
-        fab = NcclFabric(world, rank, layout.group_width(topo), dev)
+        Fab = PeerFabric if kind == "peer" else NcclFabric
+        fab = Fab(world, rank, layout.group_width(topo), dev)
         dist_model = SPTT(topo, layout, placement, assignment, pooling, B, fab, tm=cfg, dtype=torch.float32,
                           device=dev, lr=0.05)
         # reference: every rank on this GPU through the loopback fabric
@@ -73,10 +74,12 @@ def _worker(rank, world, port, hosts, rph, q):
         gen = np.random.default_rng(5)
         O = dist_model.plan.out_width()
         grads = {r: torch.from_numpy(gen.normal(size=(B, O)).astype(np.float32)).to(dev) for r in range(world)}
-        out_d = dist_model.train_step({rank: kjts[rank]}, {rank: grads[rank]})
-        out_r = ref.train_step(kjts2, grads)
-        torch.cuda.synchronize()
-        ok = torch.allclose(out_d[rank], out_r[rank], rtol=1e-6, atol=1e-6)
+        ok = True
+        for _ in range(steps):  # several steps: peer-written buffers are reused
+            out_d = dist_model.train_step({rank: kjts[rank]}, {rank: grads[rank]})
+            out_r = ref.train_step(kjts2, grads)
+            torch.cuda.synchronize()
+            ok = ok and torch.allclose(out_d[rank], out_r[rank], rtol=1e-6, atol=1e-6)
         for sid in dist_model.engine.weights:
             ok = ok and torch.allclose(dist_model.engine.weights[sid], ref.engine.weights[sid], rtol=1e-5,
                                        atol=1e-6)
@@ -89,8 +92,9 @@ def _worker(rank, world, port, hosts, rph, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("hosts,rph", [(2, 1), (2, 2), (4, 1)])
-def test_distributed_step_matches_loopback(hosts, rph):
+@pytest.mark.parametrize("kind,steps", [("nccl", 1), ("peer", 3)])
+@pytest.mark.parametrize("hosts,rph", [(2, 1), (1, 2), (2, 2), (4, 1), (1, 4)])
+def test_distributed_step_matches_loopback(hosts, rph, kind, steps):
     world = hosts * rph
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
@@ -99,7 +103,7 @@ def test_distributed_step_matches_loopback(hosts, rph):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, hosts, rph, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, hosts, rph, q, kind, steps)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
