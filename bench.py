@@ -201,6 +201,24 @@ def _config(args, N):
             "l2": "inputs larger than L2 (tables >= 6.6 GB bf16, uniform random rows), no flush"}
 
 
+def _traffic(args, N) -> dict:
+    """Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum)
+    of the roofline kernels from the committed ncu --set full capture of this
+    exact N=1 workload (profiles/traffic.json, written by tools/make_traffic.py);
+    {} for any other configuration."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)
+    except Exception:
+        return {}
+    want = {"gpus": 1, "tables": args.tables, "rows": args.rows, "dim": args.dim, "pool": args.pool,
+            "batch": args.batch, "tm": args.tm, "tm_out": args.tm_out, "cross_layers": args.cross_layers,
+            "dtype": args.dtype}
+    if N != 1 or any(t.get("config", {}).get(k) != v for k, v in want.items()):
+        return {}
+    return t.get("kernels", {})
+
+
 def _towers(args, N):
     if args.towers:
         return args.towers
@@ -403,11 +421,14 @@ def main():
     except Exception:
         hbm, tf = 6650.0, 1400.0
         peak_src = "fallback (B200_PROFILING.md)"
+    traffic = _traffic(args, N)
     n_look = max(1, timers.count("lookup_fwd") // args.steps)
     look_ms = ph.get("lookup_fwd", 0.0) / n_look
     look_gbs = look_bytes / (look_ms * 1e-3) / 1e9 if look_ms else 0.0
+    tl = traffic.get("pooled_fwd", {})
     roof_lookup = {"bound": "hbm", "achieved": look_gbs, "peak": hbm, "unit": "GB/s", "frac": look_gbs / hbm,
-                   "traffic": None, "kernel": "dmt::pooled_fwd_kernel", "algorithmic_bytes": look_bytes,
+                   "traffic": tl.get("dram_bytes_per_launch"), "traffic_source": tl.get("source"),
+                   "kernel": "dmt::pooled_fwd_kernel", "algorithmic_bytes": look_bytes,
                    "launch_ms": look_ms, "peak_source": peak_src}
     roof = roof_lookup
     if tm_cfg is not None and args.tm == "dcn":
@@ -419,9 +440,17 @@ def main():
         tm_ms = ph.get("tm_fwd", 0.0) + ph.get("tm_bwd", 0.0)
         if tm_ms > look_ms:
             ach = tm_flops_step / (tm_ms * 1e-3) / 1e12
+            tg = traffic.get("gemm_dcn_step", {})
+            nl = tg.get("launches")
             roof = {"bound": "tensor", "achieved": ach, "peak": tf, "unit": "TFLOP/s", "frac": ach / tf,
-                    "traffic": None, "kernel": "dmt::gemm::gemm_kernel (DCN fwd+bwd GEMMs, per step)",
-                    "algorithmic_flops": tm_flops_step, "ms": tm_ms, "peak_source": peak_src + " bf16 sustained"}
+                    "traffic": tg.get("dram_bytes_per_launch"), "traffic_source": tg.get("source"),
+                    "kernel": "dmt::gemm::gemm_kernel (the DCN fwd+bwd GEMMs of one step)",
+                    "launches_per_step": nl,
+                    "algorithmic_flops": tm_flops_step,
+                    "algorithmic_flops_per_launch": tm_flops_step / nl if nl else None,
+                    "ms": tm_ms, "ms_note": "tm_fwd + tm_bwd phases (CUDA events): GEMMs plus the small "
+                                           "column-sum / copy kernels between them, so achieved is a lower bound",
+                    "peak_source": peak_src + " bf16 sustained"}
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

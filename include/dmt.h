@@ -210,9 +210,15 @@ enum dmt_epilogue {
    *   dx0 (+)= g * u_l             -> aux2   (fp32, accumulated if FLAG_AUX2_ACCUM)
    * with x0 = args.x0 and u_l = args.xl. */
   DMT_EPI_DCN_BWD = 4,
-  /* last DCN layer: d = acc + beta*C + aux2 (fp32 dx0)  ->  dX of the tower */
+  /* last DCN layer: d = acc + beta*C + aux2 (fp32 dx0)  ->  dX of the tower,
+   * or, with npairs > 0, d = acc + beta*C + sum_j pair_g[j] * pair_u[j]
+   * (dx0 = sum_l g_{l+1} * u_l read straight from the saved layer tensors, so
+   * the per-layer DCN_BWD epilogues need no fp32 dx0 read-modify-write:
+   * DCN_BWD with aux2 = NULL only writes g and gu). */
   DMT_EPI_DCN_FINAL = 5
 };
+
+#define DMT_GEMM_MAX_PAIRS 4
 
 /* dmt_gemm_args.flags: operand stored transposed (MN-major).  TRANS_A: `a`
  * holds A^T as a [k, m] matrix with row stride lda (m contiguous); TRANS_B:
@@ -224,7 +230,12 @@ enum dmt_gemm_flags {
   DMT_GEMM_AUX2_ACCUM = 4,
   /* acc is scaled by args.alpha before the epilogue: with DMT_EPI_ACC,
    * beta = 1 and c = d = W this is a fused SGD step W -= lr * dW (alpha = -lr) */
-  DMT_GEMM_SCALE_ACC = 8
+  DMT_GEMM_SCALE_ACC = 8,
+  /* tuning overrides (benchmarks): no L2 prefetch of the epilogue operands;
+   * force the tile width BN = 64 * ((flags & BN_MASK) >> BN_SHIFT) */
+  DMT_GEMM_NO_PREFETCH = 16,
+  DMT_GEMM_BN_SHIFT = 8,
+  DMT_GEMM_BN_MASK = 0xF00
 };
 
 typedef struct dmt_gemm_args {
@@ -246,7 +257,21 @@ typedef struct dmt_gemm_args {
   int32_t out_dtype; /* dmt_dtype of d */
   int32_t epilogue;
   int32_t flags;     /* dmt_gemm_flags */
+  /* DCN_FINAL pair sum (16-bit operands, row stride ld_x) */
+  int32_t npairs;
+  int32_t pad_;
+  const void* pair_g[DMT_GEMM_MAX_PAIRS];
+  const void* pair_u[DMT_GEMM_MAX_PAIRS];
+  /* DCN_BWD, optional: fused bias gradient.  Column sums of the stored gu per
+   * (128-row tile, 32-row quarter): fp32 [dmt_gemm_colsum_rows(m), n]; finish
+   * with dmt_column_sum_parts.  Needs n % 32 == 0 and 16-byte aligned rows. */
+  float* colsum_part;
 } dmt_gemm_args;
+
+/* rows of the colsum_part buffer for an m-row GEMM */
+int64_t dmt_gemm_colsum_rows(int64_t m);
+/* out[c] = sum_r part[r, c]  (fp64 accumulation in row order, deterministic) */
+int dmt_column_sum_parts(const float* part, int64_t rows, int64_t cols, float* out, dmt_stream_t stream);
 
 int dmt_gemm(const dmt_gemm_args* args, dmt_stream_t stream);
 

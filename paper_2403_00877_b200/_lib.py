@@ -20,6 +20,8 @@ DT_F32, DT_BF16, DT_F64, DT_F16 = 0, 1, 2, 3
 POOL_NONE, POOL_SUM, POOL_MEAN = 0, 1, 2
 EPI_NONE, EPI_BIAS, EPI_CROSS, EPI_ACC, EPI_DCN_BWD, EPI_DCN_FINAL = 0, 1, 2, 3, 4, 5
 GEMM_TRANS_A, GEMM_TRANS_B, GEMM_AUX2_ACCUM, GEMM_SCALE_ACC = 1, 2, 4, 8
+GEMM_NO_PREFETCH, GEMM_BN_SHIFT = 16, 8  # tuning overrides (benchmarks only)
+GEMM_MAX_PAIRS = 4
 OPT_SGD, OPT_ROWWISE_ADAGRAD = 0, 1
 EBIT_INDEX, EBIT_BAGLEN = 1, 2
 
@@ -61,6 +63,8 @@ class GemmArgs(C.Structure):
         ("lda", i64), ("ldb", i64), ("ld_d", i64), ("ld_x", i64),
         ("rows_per_group", i64), ("ld_group", i64),
         ("beta", f32), ("alpha", f32), ("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("flags", i32),
+        ("npairs", i32), ("pad_", i32), ("pair_g", vp * GEMM_MAX_PAIRS), ("pair_u", vp * GEMM_MAX_PAIRS),
+        ("colsum_part", vp),
     ]
 
 
@@ -89,6 +93,8 @@ _SIGS = {
     "dmt_transpose": (C.c_int, [vp, i64, i64, i64, vp, i64, i32, vp]),
     "dmt_column_sum_workspace_size": (sz, [i64, i64]),
     "dmt_column_sum": (C.c_int, [vp, i64, i64, i64, vp, i32, vp, sz, vp]),
+    "dmt_gemm_colsum_rows": (i64, [i64]),
+    "dmt_column_sum_parts": (C.c_int, [vp, i64, i64, vp, vp]),
     "dmt_cross_bwd_pointwise": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, vp]),
     "dmt_sgd_dense": (C.c_int, [vp, vp, i64, f32, i32, vp]),
     "dmt_convert": (C.c_int, [vp, i32, vp, i32, i64, vp]),

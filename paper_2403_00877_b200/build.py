@@ -22,11 +22,15 @@ LIB = os.path.join(HERE, "libdmt.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "177", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["kjt.cu", "lookup.cu", "assemble.cu", "gemm_sm100.cu"]
+SOURCES = ["gemm_kk.cu", "gemm_km.cu", "gemm_mk.cu", "gemm_mm.cu", "kjt.cu", "lookup.cu", "assemble.cu",
+           "gemm_sm100.cu"]
 
 
 def _deps(src: str) -> list[str]:
-    return [os.path.join(CSRC, src), os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "dmt.h")]
+    deps = [os.path.join(CSRC, src), os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "dmt.h")]
+    if src.startswith("gemm"):
+        deps.append(os.path.join(CSRC, "gemm_sm100.cuh"))
+    return deps
 
 
 def _stale(target: str, deps: list[str]) -> bool:

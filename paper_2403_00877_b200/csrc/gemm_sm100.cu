@@ -22,844 +22,21 @@
 // operands use kind::tf32 with the 3xTF32 split (a = a_hi + a_lo, products
 // hi*hi + hi*lo + lo*hi accumulate in TMEM), which restores ~fp32 accuracy
 // (rtol 1e-5 parity bar of the north star).
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
-#include "common.cuh"
+// The kernel and its launch / dispatch templates live in gemm_sm100.cuh; this
+// file holds the C ABI and routes to the per-majorness instantiation units.
+#include "gemm_sm100.cuh"
 
 namespace dmt {
 namespace gemm {
 
-constexpr int kEpiWarps = 8;   // two warps per TMEM lane quarter, each owns half the columns
-constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr int kBlockM = 128;
-constexpr int kAtomBytes = 128;  // one SWIZZLE_128B row = BLOCK_K bytes per stage
-constexpr int kUmmaKBytes = 32;  // K bytes consumed by one tcgen05.mma (16 x bf16 / 8 x tf32)
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-template <int KIND>  // 0 = f16/bf16, 1 = tf32
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                     uint32_t accumulate) {
-  if constexpr (KIND == 0) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-  } else {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-  }
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-// 32 lanes x 32 columns of 32-bit TMEM -> 32 registers per thread.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// SM100 shared-memory matrix descriptor, K-major, SWIZZLE_128B:
-//   [0,14) start>>4  [16,30) LBO>>4 (unused for swizzled K-major)
-//   [32,46) SBO>>4 = 1024 B between 8-row core groups   [46,48) version = 1
-//   [61,64) layout = 2 (SWIZZLE_128B)
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo = 16, uint32_t sbo = 1024) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-
-// Operand tile in shared memory (SWIZZLE_128B), ROWS x one 128-byte K block:
-//   K-major : ROWS rows of 128 B (K contiguous); 8-row groups 1024 B apart
-//             (SBO); one MMA K-step advances the start address by 32 B.
-//   MN-major: ROWS/ATOM columns of ATOM = 128/es MN-elements; each column is
-//             BK K-rows of 128 B (LBO = BK*128 B between columns, SBO = 1024 B
-//             between 8-K-row groups); one MMA K-step = 32/es K-rows =
-//             4096/es bytes.  This is how dW = G^T X and dX = G W read their
-//             operands without any transpose kernel.
-template <typename TIN, bool MN>
-struct Operand {
-  static constexpr int ES = sizeof(TIN);
-  static constexpr int BK = kAtomBytes / ES;       // K elements per stage
-  static constexpr int ATOM = kAtomBytes / ES;     // MN elements per 128-byte atom
-  static constexpr uint32_t COL_BYTES = BK * kAtomBytes;
-  __device__ static __forceinline__ uint64_t desc(uint32_t base) {
-    return MN ? make_desc(base, COL_BYTES, 1024) : make_desc(base, 16, 1024);
-  }
-  __device__ static __forceinline__ uint64_t kstep(int kk) {
-    return MN ? (uint64_t)(((uint32_t)kk * (4096u / ES)) >> 4) : (uint64_t)((kk * kUmmaKBytes) >> 4);
-  }
-  template <int ROWS>
-  __device__ static __forceinline__ void load(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0, int r0) {
-    if constexpr (!MN) {
-      tma_load_2d(dst, map, bar, k0, r0);
-    } else {
-#pragma unroll
-      for (int c = 0; c < ROWS / ATOM; ++c) tma_load_2d(dst + c * COL_BYTES, map, bar, r0 + c * ATOM, k0);
-    }
-  }
-};
-
-// Instruction descriptor (kind::f16 / kind::tf32), both operands K-major:
-//   [4,6) D fmt = 1 (f32)  [7,10) A fmt  [10,13) B fmt  [17,23) N>>3  [24,29) M>>4
-//   [15] A major (1 = MN)  [16] B major (1 = MN)
-__host__ __device__ constexpr uint32_t make_idesc(int ab_fmt, int m, int n, bool a_mn = false, bool b_mn = false) {
-  return (1u << 4) | ((uint32_t)ab_fmt << 7) | ((uint32_t)ab_fmt << 10) | ((uint32_t)(a_mn ? 1 : 0) << 15) |
-         ((uint32_t)(b_mn ? 1 : 0) << 16) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
-}
-
-struct Params {
-  int64_t m, n, k;
-  int64_t ld_d, ld_x, rows_per_group, ld_group;
-  void* d;
-  const float* bias;
-  const void* x0;
-  const void* xl;
-  void* aux;
-  const void* c;
-  float* aux2;
-  float beta;
-  float alpha;
-  int scale_acc;
-  int aux2_accum;
-  int out_dtype;
-  int in_dtype;
-  int epilogue;
-  int vec_store;
-  int vec_x;
-  int coalesced;
-};
-
-// 32 consecutive elements of one row <-> 32 fp32 registers.  The vector forms
-// need 16-byte alignment; the scalar forms are predicated (tail / unaligned).
-template <typename TX>
-__device__ __forceinline__ void load32v(const TX* __restrict__ p, float* v) {
-  if constexpr (sizeof(TX) == 4) {
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      float4 x = *reinterpret_cast<const float4*>(p + i);
-      v[i] = x.x; v[i + 1] = x.y; v[i + 2] = x.z; v[i + 3] = x.w;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; i += 8) {
-      uint4 x = *reinterpret_cast<const uint4*>(p + i);
-      const TX* h = reinterpret_cast<const TX*>(&x);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[i + j] = to_f<TX>(h[j]);
-    }
-  }
-}
-template <typename TO>
-__device__ __forceinline__ void store32v(TO* __restrict__ p, const float* v) {
-  if constexpr (sizeof(TO) == 4) {
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; i += 8) {
-      uint4 x;
-      TO* h = reinterpret_cast<TO*>(&x);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) h[j] = from_f<TO>(v[i + j]);
-      *reinterpret_cast<uint4*>(p + i) = x;
-    }
-  }
-}
-template <typename TX>
-__device__ __forceinline__ void load32s(const TX* __restrict__ p, float* v, int n) {
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = (i < n) ? to_f<TX>(p[i]) : 0.f;
-}
-template <typename TO>
-__device__ __forceinline__ void store32s(TO* __restrict__ p, const float* v, int n) {
-#pragma unroll
-  for (int i = 0; i < 32; ++i)
-    if (i < n) p[i] = from_f<TO>(v[i]);
-}
-
-// 8 consecutive elements (16 B for 16-bit types, 32 B for fp32) <-> 8 floats.
-template <typename T>
-__device__ __forceinline__ void load8(const T* __restrict__ p, float* v) {
-  if constexpr (sizeof(T) == 4) {
-    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-  } else {
-    uint4 x = *reinterpret_cast<const uint4*>(p);
-    const T* h = reinterpret_cast<const T*>(&x);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = to_f<T>(h[j]);
-  }
-}
-template <typename T>
-__device__ __forceinline__ void store8(T* __restrict__ p, const float* v) {
-  if constexpr (sizeof(T) == 4) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
-  } else {
-    uint4 x;
-    T* h = reinterpret_cast<T*>(&x);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) h[j] = from_f<T>(v[j]);
-    *reinterpret_cast<uint4*>(p) = x;
-  }
-}
-
-// Epilogue math for 8 columns of one row (coalesced path: 4 lanes per row).
-template <typename TIN, typename TO>
-__device__ __forceinline__ void epi8(const Params& p, int64_t row, int64_t col, float* v) {
-  if (p.epilogue == DMT_EPI_BIAS || p.epilogue == DMT_EPI_CROSS) {
-    float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + col));
-    float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + col + 4));
-    v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
-    v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
-  }
-  const int64_t xo = row * p.ld_x + col;
-  if (p.epilogue == DMT_EPI_CROSS) {
-    float a[8], b[8];
-    load8<TIN>(reinterpret_cast<const TIN*>(p.x0) + xo, a);
-    load8<TIN>(reinterpret_cast<const TIN*>(p.xl) + xo, b);
-    if (p.aux) store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, v);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = a[j] * v[j] + b[j];
-  } else if (p.epilogue == DMT_EPI_ACC || p.epilogue == DMT_EPI_DCN_BWD || p.epilogue == DMT_EPI_DCN_FINAL) {
-    if (p.beta != 0.f) {
-      float c[8];
-      load8<TO>(reinterpret_cast<const TO*>(p.c) + row * p.ld_d + col, c);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] += p.beta * c[j];
-    }
-    if (p.epilogue == DMT_EPI_DCN_FINAL) {
-      float d[8];
-      load8<float>(p.aux2 + xo, d);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] += d[j];
-    } else if (p.epilogue == DMT_EPI_DCN_BWD) {
-      float x0[8], u[8], d[8];
-      load8<TIN>(reinterpret_cast<const TIN*>(p.x0) + xo, x0);
-      load8<TIN>(reinterpret_cast<const TIN*>(p.xl) + xo, u);
-      if (p.aux2_accum) load8<float>(p.aux2 + xo, d);
-      else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) d[j] = 0.f;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        x0[j] *= v[j];          // gu = g * x0
-        d[j] += v[j] * u[j];    // dx0 += g * u
-      }
-      store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, x0);
-      store8<float>(p.aux2 + xo, d);
-    }
-  }
-  TO* drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
-  store8<TO>(drow + col, v);
-}
-
-// Raw (unconverted) epilogue inputs of one 8-column row piece, so two pieces'
-// loads can be in flight before either is consumed (memory-level parallelism).
-template <typename TIN, typename TO>
-struct EpiIn {
-  using RI = typename std::conditional<sizeof(TIN) == 4, float4, uint4>::type;
-  using RO = typename std::conditional<sizeof(TO) == 4, float4, uint4>::type;
-  RI x0[sizeof(TIN) == 4 ? 2 : 1], u[sizeof(TIN) == 4 ? 2 : 1];
-  RO c[sizeof(TO) == 4 ? 2 : 1];
-  float4 d[2];
-};
-
-template <typename R, typename T, int N>
-__device__ __forceinline__ void rawld(const T* p, R (&r)[N]) {
-#pragma unroll
-  for (int i = 0; i < N; ++i) r[i] = reinterpret_cast<const R*>(p)[i];
-}
-template <typename R, typename T, int N>
-__device__ __forceinline__ void rawcvt(const R (&r)[N], float* v) {
-  load8<T>(reinterpret_cast<const T*>(&r[0]), v);
-}
-
-template <typename TIN, typename TO>
-__device__ __forceinline__ void epi_load(const Params& p, int64_t row, int64_t col, EpiIn<TIN, TO>& in) {
-  const int64_t xo = row * p.ld_x + col;
-  const int e = p.epilogue;
-  if (e == DMT_EPI_CROSS || e == DMT_EPI_DCN_BWD) {
-    rawld(reinterpret_cast<const TIN*>(p.x0) + xo, in.x0);
-    rawld(reinterpret_cast<const TIN*>(p.xl) + xo, in.u);
-  }
-  if ((e == DMT_EPI_ACC || e == DMT_EPI_DCN_BWD || e == DMT_EPI_DCN_FINAL) && p.beta != 0.f)
-    rawld(reinterpret_cast<const TO*>(p.c) + row * p.ld_d + col, in.c);
-  if (e == DMT_EPI_DCN_FINAL || (e == DMT_EPI_DCN_BWD && p.aux2_accum)) rawld(p.aux2 + xo, in.d);
-}
-
-template <typename TIN, typename TO>
-__device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t col, float* v,
-                                           const EpiIn<TIN, TO>& in) {
-  const int e = p.epilogue;
-  if (e == DMT_EPI_BIAS || e == DMT_EPI_CROSS) {
-    float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + col));
-    float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + col + 4));
-    v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
-    v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
-  }
-  const int64_t xo = row * p.ld_x + col;
-  if (e == DMT_EPI_CROSS) {
-    float a[8], b[8];
-    rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.x0, a);
-    rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.u, b);
-    if (p.aux) store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, v);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = a[j] * v[j] + b[j];
-  } else if (e == DMT_EPI_ACC || e == DMT_EPI_DCN_BWD || e == DMT_EPI_DCN_FINAL) {
-    if (p.beta != 0.f) {
-      float c[8];
-      rawcvt<typename EpiIn<TIN, TO>::RO, TO>(in.c, c);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] += p.beta * c[j];
-    }
-    if (e == DMT_EPI_DCN_FINAL) {
-      float d[8];
-      rawcvt<float4, float>(in.d, d);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] += d[j];
-    } else if (e == DMT_EPI_DCN_BWD) {
-      float x0[8], u[8], d[8];
-      rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.x0, x0);
-      rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.u, u);
-      if (p.aux2_accum) rawcvt<float4, float>(in.d, d);
-      else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) d[j] = 0.f;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        x0[j] *= v[j];
-        d[j] += v[j] * u[j];
-      }
-      store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, x0);
-      store8<float>(p.aux2 + xo, d);
-    }
-  }
-  TO* drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
-  store8<TO>(drow + col, v);
-}
-
-constexpr int kStileFloats = 32 * 33;  // per-warp padded 32x32 fp32 staging tile
-
-// BN: tile N (64/128/256); NOPS: 1 (plain) or 3 (3xTF32); KIND: 0 f16-family, 1 tf32
-template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN>
-__global__ void __launch_bounds__(kThreads, 1)
-gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-            const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_lo,
-            const Params p, uint32_t idesc) {
-  constexpr int A_BYTES = kBlockM * kAtomBytes;
-  constexpr int B_BYTES = BN * kAtomBytes;
-  constexpr int NSETS = (NOPS == 3) ? 2 : 1;  // hi (+ lo) operand copies
-  constexpr int STAGE_BYTES = NSETS * (A_BYTES + B_BYTES);
-  constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* stile_all = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tiles_m = ceil_div(p.m, kBlockM), tiles_n = ceil_div(p.n, BN);
-  const int64_t num_tiles = tiles_m * tiles_n;
-  const int num_kb = (int)ceil_div(p.k * (int64_t)sizeof(TIN), kAtomBytes);
-  constexpr int K_ELEMS = kAtomBytes / sizeof(TIN);
-  using OA = Operand<TIN, AMN>;
-  using OB = Operand<TIN, BMN>;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], kEpiWarps);  // one arrive per epilogue warp
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (int)((tile / tiles_n) * kBlockM);
-        const int n0 = (int)((tile % tiles_n) * BN);
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
-          OA::template load<kBlockM>(sa, &map_a, &full[stage], kb * K_ELEMS, m0);
-          OB::template load<BN>(sb, &map_b, &full[stage], kb * K_ELEMS, n0);
-          if constexpr (NSETS == 2) {
-            uint8_t* sa2 = sb + B_BYTES;
-            uint8_t* sb2 = sa2 + A_BYTES;
-            OA::template load<kBlockM>(sa2, &map_a_lo, &full[stage], kb * K_ELEMS, m0);
-            OB::template load<BN>(sb2, &map_b_lo, &full[stage], kb * K_ELEMS, n0);
-          }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          uint8_t* sa = smem + stage * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
-          const uint64_t da = OA::desc(smem_u32(sa));
-          const uint64_t db = OB::desc(smem_u32(sb));
-#pragma unroll
-          for (int kk = 0; kk < kAtomBytes / kUmmaKBytes; ++kk) {
-            const uint64_t ada = OA::kstep(kk), adb = OB::kstep(kk);
-            const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
-            umma<KIND>(tmem_d, da + ada, db + adb, idesc, accum);
-            if constexpr (NSETS == 2) {
-              uint8_t* sa2 = sb + B_BYTES;
-              uint8_t* sb2 = sa2 + A_BYTES;
-              const uint64_t da2 = OA::desc(smem_u32(sa2));
-              const uint64_t db2 = OB::desc(smem_u32(sb2));
-              umma<KIND>(tmem_d, da + ada, db2 + adb, idesc, 1u);  // hi * lo
-              umma<KIND>(tmem_d, da2 + ada, db + adb, idesc, 1u);  // lo * hi
-            }
-          }
-          umma_commit(&empty[stage]);  // smem slot reusable once these MMAs retire
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        umma_commit(&tfull[acc]);  // accumulator complete
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;                       // TMEM lane quarter accessible to this warp
-    const int half = (warp - 2) / 4;              // which half of the tile's columns
-    constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
-    int it = 0;
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      const int64_t m0 = (tile / tiles_n) * kBlockM;
-      const int64_t n0 = (tile % tiles_n) * BN;
-      float* stile = stile_all + (warp - 2) * kStileFloats;
-      if (p.coalesced && n0 + (int64_t)(half + 1) * kColsPerWarp <= p.n) {
-        // Pipelined full-width path: the epilogue operands (x0 / u / C / dx0)
-        // do not depend on the accumulator, so the loads of slab-pair k+1 are
-        // issued before slab-pair k is finished -- and the first ones before
-        // the accumulator barrier -- hiding their latency behind the MMAs.
-        // slab k = 8 rows x 32 columns of this warp's chunk (k & 3) of chunk k >> 2
-        constexpr int kSlabs = (kColsPerWarp / 32) * 4;
-        const int c8 = (lane & 3) * 8;
-        auto slab_pos = [&](int k, int64_t& r, int64_t& col) {
-          col = n0 + half * kColsPerWarp + (k >> 2) * 32 + c8;
-          r = m0 + q * 32 + (k & 3) * 8 + (lane >> 2);
-        };
-        EpiIn<TIN, TO> nx;
-        {
-          int64_t r, col;
-          slab_pos(0, r, col);
-          if (r < p.m) epi_load<TIN, TO>(p, r, col, nx);
-        }
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-#pragma unroll 1
-        for (int k = 0; k < kSlabs; ++k) {
-          if ((k & 3) == 0) {  // stage the next 32-column chunk of the accumulator
-            float v[32];
-            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) +
-                          (uint32_t)(acc * BN + half * kColsPerWarp + (k >> 2) * 32), v);
-            if (p.scale_acc) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
-            }
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) stile[lane * 33 + i] = v[i];
-            __syncwarp();
-          }
-          EpiIn<TIN, TO> cur = nx;
-          int64_t r, col;
-          slab_pos(k, r, col);
-          if (k + 1 < kSlabs) {
-            int64_t rn, coln;
-            slab_pos(k + 1, rn, coln);
-            if (rn < p.m) epi_load<TIN, TO>(p, rn, coln, nx);
-          }
-          const int rl = (k & 3) * 8 + (lane >> 2);
-          float a[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) a[j] = stile[rl * 33 + c8 + j];
-          if (r < p.m) epi_finish<TIN, TO>(p, r, col, a, cur);
-        }
-        __syncwarp();
-        tc_fence_before();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        continue;
-      }
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const int64_t row = m0 + q * 32 + lane;
-      const bool row_ok = row < p.m;
-      TO* drow = nullptr;
-      if (row_ok)
-        drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
-#pragma unroll 1
-      for (int c = half * kColsPerWarp; c < (half + 1) * kColsPerWarp; c += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), v);
-        if (p.scale_acc) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
-        }
-        const int64_t col = n0 + c;
-        const int64_t rem = p.n - col;
-        const int ncols = rem <= 0 ? 0 : (rem < 32 ? (int)rem : 32);
-        if (ncols == 0) continue;  // warp-uniform
-        if (ncols == 32 && p.coalesced) {
-          // stage the 32x32 chunk (thread = row) through a padded smem tile,
-          // then 4 lanes per row: every global access of the warp covers 8
-          // rows x 64-128 contiguous bytes instead of 32 scattered rows.
-#pragma unroll
-          for (int i = 0; i < 32; ++i) stile[lane * 33 + i] = v[i];
-          __syncwarp();
-          const int c8 = (lane & 3) * 8;
-#pragma unroll 1
-          for (int it = 0; it < 4; it += 2) {
-            // two 8-row slabs per pass: both slabs' inputs are loaded before
-            // either is consumed
-            const int rl0 = it * 8 + (lane >> 2), rl1 = rl0 + 8;
-            const int64_t r0 = m0 + q * 32 + rl0, r1 = r0 + 8;
-            EpiIn<TIN, TO> in0, in1;
-            if (r0 < p.m) epi_load<TIN, TO>(p, r0, col + c8, in0);
-            if (r1 < p.m) epi_load<TIN, TO>(p, r1, col + c8, in1);
-            float a[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) a[j] = stile[rl0 * 33 + c8 + j];
-            if (r0 < p.m) epi_finish<TIN, TO>(p, r0, col + c8, a, in0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) a[j] = stile[rl1 * 33 + c8 + j];
-            if (r1 < p.m) epi_finish<TIN, TO>(p, r1, col + c8, a, in1);
-          }
-          __syncwarp();
-          continue;
-        }
-        if (!row_ok) continue;
-        const bool full = ncols == 32;
-        if (p.epilogue == DMT_EPI_BIAS || p.epilogue == DMT_EPI_CROSS) {
-          if (full) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              float4 bb = __ldg(reinterpret_cast<const float4*>(p.bias + col + i));
-              v[i] += bb.x; v[i + 1] += bb.y; v[i + 2] += bb.z; v[i + 3] += bb.w;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += (i < ncols) ? p.bias[col + i] : 0.f;
-          }
-        }
-        if (p.epilogue == DMT_EPI_CROSS) {
-          const TIN* x0p = reinterpret_cast<const TIN*>(p.x0) + row * p.ld_x + col;
-          const TIN* xlp = reinterpret_cast<const TIN*>(p.xl) + row * p.ld_x + col;
-          TIN* auxp = p.aux ? reinterpret_cast<TIN*>(p.aux) + row * p.ld_x + col : nullptr;
-          float t[32];
-          if (full && p.vec_x) {
-            if (auxp) store32v<TIN>(auxp, v);
-            load32v<TIN>(x0p, t);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= t[i];
-            load32v<TIN>(xlp, t);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += t[i];
-          } else {
-            if (auxp) store32s<TIN>(auxp, v, ncols);
-            load32s<TIN>(x0p, t, ncols);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= t[i];
-            load32s<TIN>(xlp, t, ncols);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += t[i];
-          }
-        } else if (p.epilogue == DMT_EPI_ACC || p.epilogue == DMT_EPI_DCN_BWD || p.epilogue == DMT_EPI_DCN_FINAL) {
-          if (p.beta != 0.f) {
-            const TO* cp = reinterpret_cast<const TO*>(p.c) + row * p.ld_d + col;
-            float t[32];
-            if (full && p.vec_store) load32v<TO>(cp, t);
-            else load32s<TO>(cp, t, ncols);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += p.beta * t[i];
-          }
-          if (p.epilogue != DMT_EPI_ACC) {
-            float* dxp = p.aux2 + row * p.ld_x + col;
-            const bool vx = full && p.vec_x;
-            if (p.epilogue == DMT_EPI_DCN_FINAL) {
-              float t[32];
-              if (vx) load32v<float>(dxp, t);
-              else load32s<float>(dxp, t, ncols);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] += t[i];
-            } else {
-              // g = v; gu = g * x0 -> aux; dx0 (+)= g * u -> aux2
-              const TIN* x0p = reinterpret_cast<const TIN*>(p.x0) + row * p.ld_x + col;
-              const TIN* up = reinterpret_cast<const TIN*>(p.xl) + row * p.ld_x + col;
-              TIN* gup = reinterpret_cast<TIN*>(p.aux) + row * p.ld_x + col;
-              float t[32], w[32];
-              if (vx) load32v<TIN>(x0p, t);
-              else load32s<TIN>(x0p, t, ncols);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) w[i] = v[i] * t[i];
-              if (vx) store32v<TIN>(gup, w);
-              else store32s<TIN>(gup, w, ncols);
-              if (vx) load32v<TIN>(up, t);
-              else load32s<TIN>(up, t, ncols);
-              if (p.aux2_accum) {
-                if (vx) load32v<float>(dxp, w);
-                else load32s<float>(dxp, w, ncols);
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) w[i] = 0.f;
-              }
-#pragma unroll
-              for (int i = 0; i < 32; ++i) w[i] += v[i] * t[i];
-              if (vx) store32v<float>(dxp, w);
-              else store32s<float>(dxp, w, ncols);
-            }
-          }
-        }
-        if (full && p.vec_store) store32v<TO>(drow + col, v);
-        else store32s<TO>(drow + col, v, ncols);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-    }
-  }
-
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
-  }
-}
-
-// ---------------------------------------------------------------- host ------
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return nullptr;
-    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
-}
-
-// K-major operand [rows, k] (row stride ld): box {128 B of K, box_rows}.
-// MN-major operand stored [k, rows] (row stride ld): box {128 B of MN, 128 B / es K-rows}.
-static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int64_t ld, int dtype,
-                     int box_rows, bool mn = false) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  CUtensorMapDataType t;
-  size_t es = dtype_size(dtype);
-  switch (dtype) {
-    case DMT_BF16: t = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16; break;
-    case DMT_F16: t = CU_TENSOR_MAP_DATA_TYPE_FLOAT16; break;
-    case DMT_F32: t = CU_TENSOR_MAP_DATA_TYPE_FLOAT32; break;
-    default: return false;
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
-  cuuint32_t box[2] = {(cuuint32_t)(kAtomBytes / es), (cuuint32_t)box_rows};
-  if (mn) {
-    dims[0] = (cuuint64_t)rows;
-    dims[1] = (cuuint64_t)k;
-    box[0] = (cuuint32_t)(kAtomBytes / es);
-    box[1] = (cuuint32_t)(kAtomBytes / es);
-  }
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, t, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN>
-static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cudaStream_t s) {
-  constexpr int NSETS = (NOPS == 3) ? 2 : 1;
-  constexpr int STAGE_BYTES = NSETS * (kBlockM + BN) * kAtomBytes;
-  constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
-                          (size_t)kEpiWarps * kStileFloats * 4 /*epilogue staging*/;
-  static_assert(SMEM <= 232448, "smem");
-  CUtensorMap ma, mb, mal, mbl;
-  if (!make_map(&ma, a->a, a->m, a->k, a->lda, a->in_dtype, kBlockM, AMN)) return DMT_ERR_CUDA;
-  if (!make_map(&mb, a->b, a->n, a->k, a->ldb, a->in_dtype, BN, BMN)) return DMT_ERR_CUDA;
-  if (NSETS == 2) {
-    if (!make_map(&mal, a_lo, a->m, a->k, a->lda, a->in_dtype, kBlockM, AMN)) return DMT_ERR_CUDA;
-    if (!make_map(&mbl, b_lo, a->n, a->k, a->ldb, a->in_dtype, BN, BMN)) return DMT_ERR_CUDA;
-  } else {
-    mal = ma;
-    mbl = mb;
-  }
-  Params p;
-  p.m = a->m; p.n = a->n; p.k = a->k;
-  p.ld_d = a->ld_d; p.ld_x = a->ld_x;
-  p.rows_per_group = a->rows_per_group > 0 ? a->rows_per_group : a->m + 1;
-  p.ld_group = a->ld_group;
-  p.d = a->d; p.bias = a->bias; p.x0 = a->x0; p.xl = a->xl; p.aux = a->aux;
-  p.c = a->c ? a->c : a->d;
-  p.aux2 = a->aux2;
-  p.aux2_accum = (a->flags & DMT_GEMM_AUX2_ACCUM) != 0;
-  p.scale_acc = (a->flags & DMT_GEMM_SCALE_ACC) != 0;
-  p.alpha = a->alpha;
-  p.beta = a->beta; p.out_dtype = a->out_dtype; p.in_dtype = a->in_dtype; p.epilogue = a->epilogue;
-  size_t eo = dtype_size(a->out_dtype);
-  p.vec_store = ((uintptr_t)a->d % 16 == 0) && ((a->ld_d * eo) % 16 == 0) && ((a->ld_group * eo) % 16 == 0);
-  size_t ei = dtype_size(a->in_dtype);
-  p.vec_x = ((uintptr_t)a->x0 % 16 == 0) && ((uintptr_t)a->xl % 16 == 0) && ((uintptr_t)a->aux % 16 == 0) &&
-            ((uintptr_t)a->aux2 % 16 == 0) && ((a->ld_x * ei) % 16 == 0) && ((a->ld_x * 4) % 16 == 0);
-  p.vec_store = p.vec_store && ((uintptr_t)p.c % 16 == 0);
-  const bool needs_x = a->epilogue == DMT_EPI_CROSS || a->epilogue == DMT_EPI_DCN_BWD || a->epilogue == DMT_EPI_DCN_FINAL;
-  p.coalesced = p.vec_store && (!needs_x || p.vec_x);
-  if (a->bias && ((uintptr_t)a->bias % 16)) return DMT_ERR_UNSUPPORTED;
-  auto kern = gemm_kernel<BN, NOPS, KIND, STAGES, TIN, TO, AMN, BMN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    if (e != cudaSuccess) {
-      set_last_error(e);
-      return DMT_ERR_CUDA;
-    }
-    attr_set = true;
-  }
-  int64_t tiles = ceil_div(a->m, kBlockM) * ceil_div(a->n, BN);
-  int grid = (int)std::min<int64_t>(tiles, DMT_NUM_SMS);
-  const int fmt = (KIND == 1) ? 2 : (std::is_same<TIN, __half>::value ? 0 : 1);
-  uint32_t idesc = make_idesc(fmt, kBlockM, BN, AMN, BMN);
-  kern<<<grid, kThreads, SMEM, s>>>(ma, mb, mal, mbl, p, idesc);
-  DMT_CHECK_LAUNCH();
-  return DMT_OK;
-}
-
-template <typename TIN, typename TO, bool AMN, bool BMN>
-static int dispatch_n(const dmt_gemm_args* a, const void* alo, const void* blo, cudaStream_t s) {
-  if constexpr (std::is_same<TIN, float>::value) {
-    if (a->n <= 64) return launch<64, 3, 1, 4, TIN, TO, AMN, BMN>(a, alo, blo, s);
-    return launch<128, 3, 1, 3, TIN, TO, AMN, BMN>(a, alo, blo, s);
-  } else {
-    if (a->n <= 64) return launch<64, 1, 0, 8, TIN, TO, AMN, BMN>(a, alo, blo, s);
-    if (a->n <= 128) return launch<128, 1, 0, 6, TIN, TO, AMN, BMN>(a, alo, blo, s);
-    return launch<256, 1, 0, 4, TIN, TO, AMN, BMN>(a, alo, blo, s);
-  }
-}
-
-template <typename TIN, typename TO>
 static int dispatch_major(const dmt_gemm_args* a, const void* alo, const void* blo, cudaStream_t s) {
   const bool amn = (a->flags & DMT_GEMM_TRANS_A) != 0, bmn = (a->flags & DMT_GEMM_TRANS_B) != 0;
-  if (!amn && !bmn) return dispatch_n<TIN, TO, false, false>(a, alo, blo, s);
-  if (amn && bmn) return dispatch_n<TIN, TO, true, true>(a, alo, blo, s);
-  if (bmn) return dispatch_n<TIN, TO, false, true>(a, alo, blo, s);
-  return dispatch_n<TIN, TO, true, false>(a, alo, blo, s);
+  if (!amn && !bmn) return gemm_major_kk(a, alo, blo, s);
+  if (amn && bmn) return gemm_major_mm(a, alo, blo, s);
+  if (bmn) return gemm_major_km(a, alo, blo, s);
+  return gemm_major_mk(a, alo, blo, s);
 }
 
-template <typename TIN>
-static int dispatch_out(const dmt_gemm_args* a, const void* alo, const void* blo, cudaStream_t s) {
-  switch (a->out_dtype) {
-    case DMT_F32: return dispatch_major<TIN, float>(a, alo, blo, s);
-    case DMT_BF16: return dispatch_major<TIN, __nv_bfloat16>(a, alo, blo, s);
-    case DMT_F16: return dispatch_major<TIN, __half>(a, alo, blo, s);
-    default: return DMT_ERR_UNSUPPORTED;
-  }
-}
 
 __global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo,
                                   int64_t n) {
@@ -871,10 +48,46 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict
   }
 }
 
+// out[c] = sum_r part[r, c] (fp64), the last step of the bias gradients the
+// DCN backward epilogues fold per (tile, quarter).  Block = 32 columns x 8 row
+// groups; group g sums rows g, g+8, ... in order, then the 8 group sums are
+// added in group order: a fixed reduction tree, so the result is
+// deterministic, with 8 x 32 independent load streams per block.
+__global__ void colsum_parts_kernel(const float* __restrict__ part, int64_t rows, int64_t cols,
+                                    float* __restrict__ out) {
+  __shared__ double red[8][33];
+  const int cx = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + cx;
+  double acc = 0.0;
+  if (c < cols) {
+#pragma unroll 4
+    for (int64_t r = g; r < rows; r += 8) acc += (double)__ldg(part + r * cols + c);
+  }
+  red[g][cx] = acc;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    double t = red[0][cx];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) t += red[i][cx];
+    out[c] = (float)t;
+  }
+}
+
 }  // namespace gemm
 }  // namespace dmt
 
 extern "C" {
+
+int64_t dmt_gemm_colsum_rows(int64_t m) { return 4 * dmt::ceil_div(m, (int64_t)dmt::gemm::kBlockM); }
+
+int dmt_column_sum_parts(const float* part, int64_t rows, int64_t cols, float* out, dmt_stream_t stream) {
+  if (rows < 0 || cols < 0) return DMT_ERR_SHAPE;
+  if (cols == 0) return DMT_OK;
+  dmt::gemm::colsum_parts_kernel<<<(unsigned)dmt::ceil_div(cols, (int64_t)32), 256, 0, (cudaStream_t)stream>>>(
+      part, rows, cols, out);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
 
 int dmt_gemm_ex(const dmt_gemm_args* args, const void* a_lo, const void* b_lo, dmt_stream_t stream) {
   using namespace dmt;
@@ -891,19 +104,24 @@ int dmt_gemm_ex(const dmt_gemm_args* args, const void* a_lo, const void* b_lo, d
     return DMT_ERR_UNSUPPORTED;
   if ((a->epilogue == DMT_EPI_BIAS || a->epilogue == DMT_EPI_CROSS) && !a->bias) return DMT_ERR_DOMAIN;
   if (a->epilogue == DMT_EPI_CROSS && (!a->x0 || !a->xl)) return DMT_ERR_DOMAIN;
-  if (a->epilogue == DMT_EPI_DCN_BWD && (!a->x0 || !a->xl || !a->aux || !a->aux2)) return DMT_ERR_DOMAIN;
-  if (a->epilogue == DMT_EPI_DCN_FINAL && !a->aux2) return DMT_ERR_DOMAIN;
+  if (a->epilogue == DMT_EPI_DCN_BWD && (!a->x0 || !a->aux || (a->aux2 && !a->xl))) return DMT_ERR_DOMAIN;
+  if (a->npairs < 0 || a->npairs > DMT_GEMM_MAX_PAIRS) return DMT_ERR_DOMAIN;
+  if (a->npairs && a->epilogue != DMT_EPI_DCN_FINAL) return DMT_ERR_DOMAIN;
+  for (int j = 0; j < a->npairs; ++j)
+    if (!a->pair_g[j] || !a->pair_u[j]) return DMT_ERR_DOMAIN;
+  if (a->npairs && a->ld_x <= 0) return DMT_ERR_UNSUPPORTED;
+  if (a->epilogue == DMT_EPI_DCN_FINAL && !a->aux2 && !a->npairs) return DMT_ERR_DOMAIN;
   if ((a->epilogue == DMT_EPI_DCN_BWD || a->epilogue == DMT_EPI_DCN_FINAL) && a->out_dtype != a->in_dtype)
     return DMT_ERR_UNSUPPORTED;
   if (a->epilogue > DMT_EPI_DCN_FINAL || a->epilogue < 0) return DMT_ERR_DOMAIN;
   cudaStream_t s = (cudaStream_t)stream;
   switch (a->in_dtype) {
-    case DMT_BF16: return gemm::dispatch_out<__nv_bfloat16>(a, nullptr, nullptr, s);
-    case DMT_F16: return gemm::dispatch_out<__half>(a, nullptr, nullptr, s);
+    case DMT_BF16: return gemm::dispatch_major(a, nullptr, nullptr, s);
+    case DMT_F16: return gemm::dispatch_major(a, nullptr, nullptr, s);
     case DMT_F32:
       if (!a_lo || !b_lo) return DMT_ERR_DOMAIN;
       if (((uintptr_t)a_lo & 15) || ((uintptr_t)b_lo & 15)) return DMT_ERR_UNSUPPORTED;
-      return gemm::dispatch_out<float>(a, a_lo, b_lo, s);
+      return gemm::dispatch_major(a, a_lo, b_lo, s);
     default: return DMT_ERR_UNSUPPORTED;
   }
 }

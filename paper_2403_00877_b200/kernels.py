@@ -330,12 +330,15 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[
          epilogue: int = L.EPI_NONE, x0=None, xl=None, aux=None, beta: float = 0.0,
          rows_per_group: int = 0, ld_group: int = 0, ld_d: Optional[int] = None,
          b_split=None, trans_a: bool = False, trans_b: bool = False, c=None, aux2=None,
-         aux2_accum: bool = False, alpha: Optional[float] = None) -> torch.Tensor:
+         aux2_accum: bool = False, alpha: Optional[float] = None, tune_flags: int = 0,
+         pairs=(), colsum_part: Optional[torch.Tensor] = None) -> torch.Tensor:
     """out[m, n] = epi(sum_k A[m, k] B[n, k]) on tcgen05 (bf16/f16 -> kind::f16,
     fp32 -> 3xTF32).  A = a (m, k), or a^T when ``trans_a`` (a stored (k, m));
     B = b (n, k), or b^T when ``trans_b`` (b stored (k, n)).  Transposed
     operands are read MN-major by TMA (no transpose pass).  ``b_split`` may
-    carry a cached (hi, lo) tf32 split of an fp32 b."""
+    carry a cached (hi, lo) tf32 split of an fp32 b.  ``pairs`` [(g, u), ...]
+    adds sum g*u in the DCN_FINAL epilogue; ``colsum_part`` receives the fused
+    per-tile column sums of gu (DCN_BWD; finish with column_sum_parts)."""
     if a.dim() != 2 or b.dim() != 2:
         raise ShapeError("gemm operands must be 2-D")
     m, k = (a.shape[1], a.shape[0]) if trans_a else (a.shape[0], a.shape[1])
@@ -370,16 +373,36 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[
     if bias is not None and (bias.dtype != torch.float32 or not bias.is_contiguous()):
         bias = bias.float().contiguous()
     flags = ((L.GEMM_TRANS_A if trans_a else 0) | (L.GEMM_TRANS_B if trans_b else 0)
-             | (L.GEMM_AUX2_ACCUM if aux2_accum else 0) | (L.GEMM_SCALE_ACC if alpha is not None else 0))
+             | (L.GEMM_AUX2_ACCUM if aux2_accum else 0) | (L.GEMM_SCALE_ACC if alpha is not None else 0)
+             | tune_flags)
     args = L.GemmArgs(
         a=a.data_ptr(), b=b.data_ptr(), d=out.data_ptr(), bias=L.ptr(bias), x0=L.ptr(x0), xl=L.ptr(xl),
         aux=L.ptr(aux), c=L.ptr(c), aux2=L.ptr(aux2), m=m, n=n, k=k, lda=a.stride(0), ldb=b.stride(0),
         ld_d=ld_d if ld_d is not None else out.stride(0),
-        ld_x=(x0.stride(0) if x0 is not None else (aux2.stride(0) if aux2 is not None else 0)),
+        ld_x=(x0.stride(0) if x0 is not None else (aux2.stride(0) if aux2 is not None else
+                                                   (pairs[0][0].stride(0) if pairs else 0))),
         rows_per_group=rows_per_group, ld_group=ld_group,
         beta=beta, alpha=alpha if alpha is not None else 1.0, in_dtype=in_dt, out_dtype=_dt(out),
-        epilogue=epilogue, flags=flags)
+        epilogue=epilogue, flags=flags, npairs=len(pairs), colsum_part=L.ptr(colsum_part))
+    if len(pairs) > L.GEMM_MAX_PAIRS:
+        raise DomainError(f"at most {L.GEMM_MAX_PAIRS} epilogue pairs")
+    for j, (g, u) in enumerate(pairs):
+        args.pair_g[j], args.pair_u[j] = g.data_ptr(), u.data_ptr()
     L.check(L.lib().dmt_gemm_ex(C.byref(args), L.ptr(a_lo), L.ptr(b_lo), L.stream_ptr()), "dmt_gemm")
+    return out
+
+
+def colsum_rows(m: int) -> int:
+    return int(L.lib().dmt_gemm_colsum_rows(m))
+
+
+def column_sum_parts(part: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """out[c] = sum_r part[r, c] (fp64 in row order): finishes fused bias grads."""
+    rows, cols = part.shape
+    if out is None:
+        out = torch.empty(cols, dtype=torch.float32, device=part.device)
+    L.check(L.lib().dmt_column_sum_parts(part.data_ptr(), rows, cols, out.data_ptr(), L.stream_ptr()),
+            "dmt_column_sum_parts")
     return out
 
 

@@ -11,6 +11,8 @@ gradients (summed over the tower's data-parallel ranks by the caller).
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 from typing import Optional
 
@@ -150,6 +152,12 @@ def interaction_pairs(num_features: int, num_towers: int, reduction_ratio: float
 # device tower module
 # --------------------------------------------------------------------------- #
 class TowerModule:
+    # DCN backward form: "accumulate" (fp32 dx0 read-modify-written by every
+    # layer's epilogue; the faster one on B200) or "pairs" (no dx0: every g_l
+    # kept, pair-sum final epilogue, bias-gradient column sums fused into the
+    # epilogues; L <= 4) -- both parity-tested
+    dcn_bwd_form = os.environ.get("DMT_DCN_BWD", "accumulate")
+
     """Device TM of one tower: forward / backward / SGD on libdmt GEMMs.
 
     Input X is (rows, F*N) in the compute dtype, rows = T*B on an SPTT rank
@@ -307,23 +315,80 @@ class TowerModule:
                 self.grads[name] = K.gemm(a, b, torch.empty(self.w[name].shape, dtype=f32, device=dev),
                                           trans_a=True, trans_b=True)
 
+        if L_ <= L.GEMM_MAX_PAIRS and self.dcn_bwd_form == "pairs":
+            return self._dcn_bwd_pairs(gy, weight_grad)
         g = torch.empty((rows, M), dtype=self.dtype, device=dev)
         gu = [torch.empty((rows, M), dtype=self.dtype, device=dev) for _ in range(2)]
         dx0 = torch.empty((rows, M), dtype=f32, device=dev)
+        # separate bias-gradient column sums: folding them into these epilogues
+        # measured slower (+45 us per layer vs 34 us for the standalone pass)
+        part = None
+
+        def bias_grad(name, t):
+            self.grads[name] = K.column_sum_parts(part) if part is not None else K.column_sum(t)
+
         K.gemm(gy, self.w["w_proj"], g, trans_b=True, epilogue=L.EPI_DCN_BWD, x0=x0, xl=us[L_ - 1],
-               aux=gu[(L_ - 1) % 2], aux2=dx0, aux2_accum=False)
+               aux=gu[(L_ - 1) % 2], aux2=dx0, aux2_accum=False, colsum_part=part)
         weight_grad("w_proj", gy, xs[-1])
         self.grads["b_proj"] = K.column_sum(gy)
         dx = torch.empty_like(g)
         for layer in range(L_ - 1, -1, -1):
             cur = gu[layer % 2]
+            bias_grad(f"b{layer}", cur)  # before the next GEMM overwrites the partials
             if layer > 0:
                 K.gemm(cur, self.w[f"w{layer}"], g, trans_b=True, epilogue=L.EPI_DCN_BWD, c=g, beta=1.0, x0=x0,
-                       xl=us[layer - 1], aux=gu[(layer - 1) % 2], aux2=dx0, aux2_accum=True)
+                       xl=us[layer - 1], aux=gu[(layer - 1) % 2], aux2=dx0, aux2_accum=True, colsum_part=part)
             else:
                 K.gemm(cur, self.w["w0"], dx, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=g, beta=1.0, aux2=dx0)
             weight_grad(f"w{layer}", cur, xs[layer])
-            self.grads[f"b{layer}"] = K.column_sum(cur)
+        return dx
+
+    def _colsum_part(self, rows, M, dev):
+        """Buffer of the fused bias-gradient partials (DCN_BWD epilogue), or None
+        when the width does not allow the fused form (M % 32 != 0)."""
+        if M % 32:
+            return None
+        key = (rows, M)
+        if getattr(self, "_part_key", None) != key:
+            self._part = torch.empty((K.colsum_rows(rows), M), dtype=torch.float32, device=dev)
+            self._part_key = key
+        return self._part
+
+    def _dcn_bwd_pairs(self, gy, weight_grad):
+        """Crossnet backward without an fp32 dx0 accumulator (L <= 4 layers):
+            g_L = gy Wp;  gu_l = g_{l+1} * x0;  g_l = gu_l W_l + g_{l+1}
+            dX = gu_0 W_0 + g_1 + sum_l g_{l+1} * u_l     (one DCN_FINAL epilogue)
+        Every g_l is kept (bf16), so the per-layer epilogues move 8 bytes per
+        element (x0, g_{l+1} in; g_l, gu out) instead of 18, and the bias
+        gradients colsum(gu_l) are folded in the same epilogues (per-tile
+        partials + one deterministic reduce) when the width is a multiple of 32."""
+        xs, us = self._saved
+        x0 = xs[0]
+        rows, M = x0.shape
+        L_ = self.cfg.cross_layers
+        dev, dt = x0.device, self.dtype
+        G = [None] + [torch.empty((rows, M), dtype=dt, device=dev) for _ in range(L_)]
+        gu = [torch.empty((rows, M), dtype=dt, device=dev) for _ in range(2)]
+        part = self._colsum_part(rows, M, dev)
+
+        def bias_grad(name, t):
+            self.grads[name] = K.column_sum_parts(part) if part is not None else K.column_sum(t)
+
+        K.gemm(gy, self.w["w_proj"], G[L_], trans_b=True, epilogue=L.EPI_DCN_BWD, x0=x0, aux=gu[(L_ - 1) % 2],
+               colsum_part=part)
+        weight_grad("w_proj", gy, xs[-1])
+        self.grads["b_proj"] = K.column_sum(gy)
+        dx = torch.empty_like(x0)
+        for layer in range(L_ - 1, -1, -1):
+            cur = gu[layer % 2]
+            bias_grad(f"b{layer}", cur)  # before the next GEMM overwrites the partials
+            if layer > 0:
+                K.gemm(cur, self.w[f"w{layer}"], G[layer], trans_b=True, epilogue=L.EPI_DCN_BWD, c=G[layer + 1],
+                       beta=1.0, x0=x0, aux=gu[(layer - 1) % 2], colsum_part=part)
+            else:
+                K.gemm(cur, self.w["w0"], dx, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=G[1], beta=1.0,
+                       pairs=[(G[j + 1], us[j]) for j in range(L_)])
+            weight_grad(f"w{layer}", cur, xs[layer])
         return dx
 
     def sgd_step(self, lr: float) -> None:

@@ -74,16 +74,24 @@ def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1):
         gen = np.random.default_rng(5)
         O = dist_model.plan.out_width()
         grads = {r: torch.from_numpy(gen.normal(size=(B, O)).astype(np.float32)).to(dev) for r in range(world)}
-        ok = True
+        # The tower all-reduce of the TM weight gradients sums W contributions
+        # in NCCL's ring order; the loopback engine sums them in rank order.
+        # For W <= 2 the two agree bit for bit (fp add commutes); for W > 2 the
+        # TM weights of step 2+ differ by fp32 reassociation, so later outputs
+        # are held to the north-star fp32 tolerance (rtol 1e-5) instead.
+        W = layout.group_width(topo)
+        tol = 1e-6 if W <= 2 else 1e-5
+        ok, worst = True, 0.0
         for _ in range(steps):  # several steps: peer-written buffers are reused
             out_d = dist_model.train_step({rank: kjts[rank]}, {rank: grads[rank]})
             out_r = ref.train_step(kjts2, grads)
             torch.cuda.synchronize()
-            ok = ok and torch.allclose(out_d[rank], out_r[rank], rtol=1e-6, atol=1e-6)
+            worst = max(worst, float((out_d[rank] - out_r[rank]).abs().max()))
+            ok = ok and torch.allclose(out_d[rank], out_r[rank], rtol=tol, atol=tol)
         for sid in dist_model.engine.weights:
             ok = ok and torch.allclose(dist_model.engine.weights[sid], ref.engine.weights[sid], rtol=1e-5,
                                        atol=1e-6)
-        q.put((rank, bool(ok), None))
+        q.put((rank, bool(ok), None if ok else f"max |out diff| {worst:.3e} (tol {tol})"))
     except Exception:  # pragma: no cover
         import traceback
 

@@ -78,7 +78,7 @@ def test_embedding_backward_is_deterministic():
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
 
 
-def _tm_objects(kind, F, N, dt, seed=0):
+def _tm_objects(kind, F, N, dt, seed=0, layers=3):
     import paper_2403_00877_b200 as P
 
     if kind == "dlrm":
@@ -86,19 +86,29 @@ def _tm_objects(kind, F, N, dt, seed=0):
         ocfg = {"kind": "dlrm", "out_dim": 16, "per_feature_outputs": 2, "flat_outputs": 1, "cross_layers": 3,
                 "seed": seed}
     else:
-        cfg = P.TMConfig(kind="dcn", out_dim=16, cross_layers=3, seed=seed)
-        ocfg = {"kind": "dcn", "out_dim": 16, "per_feature_outputs": 1, "flat_outputs": 0, "cross_layers": 3,
+        cfg = P.TMConfig(kind="dcn", out_dim=16, cross_layers=layers, seed=seed)
+        ocfg = {"kind": "dcn", "out_dim": 16, "per_feature_outputs": 1, "flat_outputs": 0, "cross_layers": layers,
                 "seed": seed}
     w = P.init_tm_weights(cfg, F, N, salt=1)
     ow = oracle.init_tm_weights(ocfg, F, N, salt=1)
     return P.TowerModule(cfg, F, N, w, dtype=dt), ocfg, ow
 
 
-@pytest.mark.parametrize("kind", ["dlrm", "dcn"])
+# DCN variants: 3 layers / width 192 = pair-sum final epilogue + fused bias
+# column sums; width 48 = pair sum on the unaligned epilogue path with separate
+# column sums; 5 layers = the fp32 dx0-accumulator form (more than 4 pairs).
+@pytest.mark.parametrize("kind,F,N,layers", [("dlrm", 6, 32, 3), ("dcn", 6, 32, 3), ("dcn", 3, 16, 3),
+                                             ("dcn", 6, 32, 5), ("dcn", 4, 32, 1)])
 @pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
-def test_tower_module_backward_vs_oracle(kind, dt):
-    F, N, rows = 6, 32, 300
-    tm, ocfg, ow = _tm_objects(kind, F, N, dt)
+@pytest.mark.parametrize("form", ["accumulate", "pairs"])
+def test_tower_module_backward_vs_oracle(kind, F, N, layers, dt, form, monkeypatch):
+    import paper_2403_00877_b200 as P
+
+    if kind == "dlrm" and form == "pairs":
+        pytest.skip("DCN-only variant")
+    monkeypatch.setattr(P.TowerModule, "dcn_bwd_form", form)
+    rows = 300
+    tm, ocfg, ow = _tm_objects(kind, F, N, dt, layers=layers)
     rng = np.random.default_rng(4)
     x = rng.normal(size=(rows, F, N)) * 0.5
     if dt == torch.bfloat16:

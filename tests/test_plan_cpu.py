@@ -150,7 +150,7 @@ def test_library_exports_every_header_symbol():
         build()
     lib = _lib.load_library(require_cuda=False)
     hdr = open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "dmt.h")).read()
-    names = set(re.findall(r"^(?:int|size_t|const char\*)\s+(dmt_\w+)\(", hdr, flags=re.M))
+    names = set(re.findall(r"^(?:int|int64_t|size_t|const char\*)\s+(dmt_\w+)\(", hdr, flags=re.M))
     assert len(names) >= 20
     for n in names:
         assert hasattr(lib, n), n

@@ -15,6 +15,17 @@ from paper_2403_00877_b200 import _lib as L  # noqa: E402
 from paper_2403_00877_b200 import kernels as K  # noqa: E402
 
 
+TUNE = [0]
+_gemm = K.gemm
+
+
+def _tuned(*a, **kw):
+    return _gemm(*a, tune_flags=TUNE[0], **kw)
+
+
+K.gemm = _tuned
+
+
 def timeit(fn, reps=20):
     for _ in range(3):
         fn()
@@ -47,6 +58,7 @@ def main():
     dW = torch.empty(M, M, device="cuda", dtype=torch.float32)
     dx0 = torch.zeros(R, M, device="cuda", dtype=torch.float32)
     gu = torch.empty(R, M, device="cuda", dtype=dt)
+    part = torch.empty(K.colsum_rows(R), M, device="cuda", dtype=torch.float32)
     cases = [
         ("fwd cross", 2 * R * M * M, lambda: K.gemm(xl, W, out, bias=b, epilogue=L.EPI_CROSS, x0=x0, xl=xl, aux=u),
          lambda: torch.matmul(xl, W.t())),
@@ -60,17 +72,35 @@ def main():
         ("bwd dX dcn_bwd", 2 * R * M * M,
          lambda: K.gemm(gu, W, out, trans_b=True, epilogue=L.EPI_DCN_BWD, c=out, beta=1.0, x0=x0, xl=u, aux=xl,
                         aux2=dx0, aux2_accum=True), lambda: torch.matmul(gu, W)),
+        ("bwd dX dcn_bwd +colsum", 2 * R * M * M,
+         lambda: K.gemm(gu, W, out, trans_b=True, epilogue=L.EPI_DCN_BWD, c=out, beta=1.0, x0=x0, xl=u, aux=xl,
+                        aux2=dx0, aux2_accum=True, colsum_part=part), None),
+        ("bwd dX final legacy", 2 * R * M * M,
+         lambda: K.gemm(gu, W, out, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=u, beta=1.0, aux2=dx0), None),
+        ("bwd dX dcn_bwd pairs", 2 * R * M * M,
+         lambda: K.gemm(gu, W, out, trans_b=True, epilogue=L.EPI_DCN_BWD, c=u, beta=1.0, x0=x0, aux=xl,
+                        colsum_part=part), None),
+        ("bwd dX final 3 pairs", 2 * R * M * M,
+         lambda: K.gemm(gu, W, out, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=u, beta=1.0,
+                        pairs=[(x0, u), (xl, u), (x0, xl)]), None),
         ("bwd dX plain (K,MN)", 2 * R * M * M, lambda: K.gemm(gu, W, out, trans_b=True), None),
         ("bwd g proj dcn_bwd", 2 * R * M * P,
          lambda: K.gemm(gy, Wp, out, trans_b=True, epilogue=L.EPI_DCN_BWD, x0=x0, xl=u, aux=xl, aux2=dx0),
          lambda: torch.matmul(gy, Wp)),
     ]
+    variants = [("auto", 0), ("nopf", L.GEMM_NO_PREFETCH)] + [
+        (f"bn{64 * j}", j << L.GEMM_BN_SHIFT) for j in (3, 4)] + [
+        (f"bn{64 * j}np", (j << L.GEMM_BN_SHIFT) | L.GEMM_NO_PREFETCH) for j in (3, 4)]
     for name, flops, fn, ref in cases:
-        ms = timeit(fn)
-        line = f"{name:22s} {ms * 1e3:8.1f} us  {flops / ms / 1e9:7.1f} TFLOP/s"
+        line = f"{name:22s}"
+        for vname, fl in variants:
+            TUNE[0] = fl
+            ms = timeit(fn)
+            line += f" {vname} {ms * 1e3:6.1f}us {flops / ms / 1e9:6.0f}TF"
+        TUNE[0] = 0
         if ref is not None:
             rms = timeit(ref)
-            line += f"   cuBLAS {rms * 1e3:8.1f} us  {flops / rms / 1e9:7.1f} TFLOP/s"
+            line += f"   cuBLAS {rms * 1e3:6.1f}us {flops / rms / 1e9:6.0f}TF"
         print(line, flush=True)
 
 

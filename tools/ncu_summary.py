@@ -1,9 +1,16 @@
 """Compact summary of an ncu report (raw page) for profiles/.
-usage: python tools/ncu_summary.py report.ncu-rep [label]"""
+usage: python tools/ncu_summary.py report.ncu-rep [label] [--json out.json]
+
+--json also writes the per-launch DRAM traffic (dram__bytes_read.sum +
+dram__bytes_write.sum) and duration of every captured launch, the source of
+bench.py's roofline "traffic" (profiles/traffic.json)."""
 import csv
 import io
+import json
 import subprocess
 import sys
+
+_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
 
 WANT = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -15,9 +22,21 @@ WANT = [
 ]
 
 
+def _val(row, h, u, name):
+    i = h.index(name)
+    return float(row[i].replace(",", "")) * _SCALE.get(u[i], 1.0)
+
+
 def main():
-    rep = sys.argv[1]
-    label = sys.argv[2] if len(sys.argv) > 2 else rep
+    argv = list(sys.argv[1:])
+    jout = None
+    if "--json" in argv:
+        k = argv.index("--json")
+        jout = argv[k + 1]
+        del argv[k:k + 2]
+    rep = argv[0]
+    label = argv[1] if len(argv) > 1 else rep
+    launches = []
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, u = rows[0], rows[1]
@@ -29,8 +48,14 @@ def main():
             if w in h:
                 i = h.index(w)
                 print(f"  {w} = {row[i]} {u[i]}")
-        rd = row[h.index("dram__bytes_read.sum")] if "dram__bytes_read.sum" in h else None
+        if "dram__bytes_read.sum" in h and "gpu__time_duration.sum" in h:
+            launches.append({"kernel": name[:160], "us": _val(row, h, u, "gpu__time_duration.sum"),
+                             "dram_bytes": _val(row, h, u, "dram__bytes_read.sum") +
+                             _val(row, h, u, "dram__bytes_write.sum")})
         print()
+    if jout:
+        with open(jout, "w") as fh:
+            json.dump({"label": label, "launches": launches}, fh, indent=1)
 
 
 if __name__ == "__main__":

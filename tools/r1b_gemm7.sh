@@ -1,0 +1,2 @@
+python tools/gemm_bench.py 16384 1664 832 > gpurun_out/gemm_t2.log 2>&1; echo rc=$?
+python tools/gemm_bench.py 8192 3328 1664 > gpurun_out/gemm_t1.log 2>&1; echo rc=$?
