@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--tm", default="dcn", choices=["dcn", "dlrm", "passthrough"])
     ap.add_argument("--tm-out", type=int, default=64)
     ap.add_argument("--cross-layers", type=int, default=3)
+    ap.add_argument("--top", default="none", choices=["none", "dcn"],
+                    help="full DCN + SPTT model: a data-parallel crossnet head to one logit + BCE loss on "
+                         "synthetic labels (instead of a synthetic upstream gradient)")
     ap.add_argument("--towers", type=int, default=0, help="0 = auto (1 at N=1, else 2)")
     ap.add_argument("--no-flat", action="store_true", help="skip the flat-baseline comparison at N>1")
     ap.add_argument("--fabric", default="peer", choices=["peer", "nccl"],
@@ -194,7 +197,7 @@ def _config(args, N):
                         f"C2 per GPU, SPTT {T} towers x {N // T} GPUs, flat all-to-all alongside",
             "tables": args.tables, "rows": args.rows, "dim": args.dim, "pooling_factor": args.pool,
             "batch_per_gpu": args.batch, "global_batch": args.batch * N, "tm": args.tm, "tm_out_dim": args.tm_out,
-            "cross_layers": args.cross_layers, "towers": T, "gpus_per_tower": N // T, "optimizer": "sgd",
+            "cross_layers": args.cross_layers, "top": args.top, "towers": T, "gpus_per_tower": N // T, "optimizer": "sgd",
             "parallelism": f"embedding model-parallel in tower, TM data-parallel in tower (T={T}, W={N // T})",
             "exchange": "loopback" if N == 1 else ("nvlink peer stores + barrier" if args.fabric == "peer"
                                                    else "nccl all-to-all"),
@@ -270,11 +273,19 @@ def main():
     fabric = make_fabric(args.fabric)
     tm_cfg = None if args.tm == "passthrough" else P.TMConfig(kind=args.tm, out_dim=args.tm_out, cross_layers=args.cross_layers,
                                                              per_feature_outputs=1, flat_outputs=0, seed=0)
+    top_cfg = (P.TMConfig(kind="dcn", out_dim=1, cross_layers=args.cross_layers, seed=0) if args.top == "dcn"
+               else None)
     model = SPTT(topo, layout, placement, assignment, pooling, B, fabric, tm=tm_cfg, dtype=dtype, device=dev,
-                 mode="sptt", lr=1e-3)
+                 mode="sptt", lr=1e-3, top=top_cfg)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     batches = [{rank: random_kjt(F, B, args.rows, Lp, gen, dev)} for _ in range(4)]
     gout = {rank: (torch.randn(B, model.out_width, generator=gen, device=dev) * 1e-3).to(dtype)}
+    labels = {rank: (torch.rand(B, generator=gen, device=dev) < 0.25).float()}  # synthetic CTR labels
+
+    def step(m, kj):
+        if m.top is not None:
+            return m.train_step_bce(kj, labels)
+        return m.train_step(kj, gout)
 
     def barrier():
         if world > 1:
@@ -283,7 +294,7 @@ def main():
     def timed_eager(m, K, Wm):
         """Eager steps with per-phase CUDA events (phase breakdown + fallback)."""
         for i in range(Wm):
-            m.train_step(batches[i % len(batches)], gout)
+            step(m, batches[i % len(batches)])
         torch.cuda.synchronize()
         barrier()
         timers = PhaseTimers()
@@ -292,7 +303,7 @@ def main():
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         for i in range(K):
-            m.train_step(batches[i % len(batches)], gout)
+            step(m, batches[i % len(batches)])
         e.record()
         torch.cuda.synchronize()
         barrier()
@@ -311,7 +322,7 @@ def main():
         (device->device, or pinned host->device for e2e) inside the region."""
         st = {rank: KJT(batches[0][rank].lengths.clone(), batches[0][rank].values.clone(),
                         batches[0][rank].nnz_per_feature, B)}
-        replay, outs = m.capture(st, gout, timers=timers)
+        replay, outs = m.capture(st, gout, timers=timers, labels=labels if m.top is not None else None)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
@@ -354,7 +365,10 @@ def main():
                 if i + 1 < n:
                     prefetch(i + 1)
                 replay()
-                torch.dot(outs[rank].view(-1).float(), gout[rank].view(-1).float(), out=loss_buf[i])
+                if m.top is not None:  # the BCE loss of this step
+                    loss_buf[i:i + 1].copy_(outs[rank])
+                else:  # <y, g> of the synthetic upstream gradient
+                    torch.dot(outs[rank].view(-1).float(), gout[rank].view(-1).float(), out=loss_buf[i])
                 losses[i:i + 1].copy_(loss_buf[i:i + 1], non_blocking=True)
 
         run(min(K, max(3, args.warmup)))  # untimed warm-up of this exact loop
@@ -438,6 +452,9 @@ def main():
         fwd = P.tm_flops(tm_cfg, Ft, Nd, rows)
         tm_flops_step = 3.0 * fwd  # fwd + (dX, dW) backward
         tm_ms = ph.get("tm_fwd", 0.0) + ph.get("tm_bwd", 0.0)
+        if top_cfg is not None:  # the head's crossnet GEMMs over the SPTT output
+            tm_flops_step += 3.0 * P.tm_flops(top_cfg, 1, model.out_width, B)
+            tm_ms += ph.get("top_fwd", 0.0) + ph.get("top_bwd", 0.0)
         if tm_ms > look_ms:
             ach = tm_flops_step / (tm_ms * 1e-3) / 1e12
             tg = traffic.get("gemm_dcn_step", {})
@@ -467,7 +484,7 @@ def main():
         del model
         torch.cuda.empty_cache()
         flat = SPTT(topo, layout, placement, assignment, pooling, B, fabric, tm=tm_cfg, dtype=dtype, device=dev,
-                    mode="flat", lr=1e-3)
+                    mode="flat", lr=1e-3, top=top_cfg)
         gout = {rank: (torch.randn(B, flat.out_width, generator=gen, device=dev) * 1e-3).to(dtype)}
         fe_ms, f_t, _ = timed_eager(flat, args.steps, args.warmup)
         fph = {k: v / args.steps for k, v in f_t.ms().items()}

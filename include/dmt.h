@@ -299,6 +299,13 @@ int dmt_cross_bwd_pointwise(const void* g, const void* x0, const void* u, void* 
                             int64_t n, int32_t dtype, dmt_stream_t stream);
 
 /* w -= lr * g  (w in dtype, g fp32), n elements */
+/* Loss head of the full DCN + SPTT training step (the reference has no
+ * training): binary cross-entropy on logits z[n],
+ * dz = scale * (sigmoid(z) - y), *loss = scale * sum BCE (one block, fixed
+ * reduction order; loss may be NULL). */
+int dmt_bce_with_logits(const void* z, const float* y, int64_t n, int32_t dtype, float scale, void* dz,
+                        float* loss, dmt_stream_t stream);
+
 int dmt_sgd_dense(void* w, const float* g, int64_t n, float lr, int32_t dtype,
                   dmt_stream_t stream);
 

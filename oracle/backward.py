@@ -25,6 +25,7 @@ __all__ = [
     "apply_sgd",
     "apply_rowwise_adagrad",
     "flat_model_grads",
+    "bce_with_logits",
 ]
 
 
@@ -122,3 +123,13 @@ def flat_model_grads(pooled_by_tower: dict, tm_cfgs: dict, tm_weights: dict, gou
         cfg = tm_cfgs.get(t) or {"kind": "passthrough"}
         d_pooled[t], d_w[t] = tm_backward(x, cfg, tm_weights.get(t), gouts[t])
     return d_pooled, d_w
+
+
+def bce_with_logits(z: np.ndarray, y: np.ndarray, scale: float):
+    """Loss head of the full model step (no reference counterpart -- parity
+    unpinned): loss = scale * sum(max(z,0) - z y + log1p(exp(-|z|))),
+    dz = scale * (sigmoid(z) - y)."""
+    z = np.asarray(z, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64).reshape(z.shape)
+    loss = scale * float(np.sum(np.maximum(z, 0) - z * y + np.log1p(np.exp(-np.abs(z)))))
+    return loss, scale * (1.0 / (1.0 + np.exp(-z)) - y)

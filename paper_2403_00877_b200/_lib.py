@@ -94,6 +94,7 @@ _SIGS = {
     "dmt_column_sum_workspace_size": (sz, [i64, i64]),
     "dmt_column_sum": (C.c_int, [vp, i64, i64, i64, vp, i32, vp, sz, vp]),
     "dmt_gemm_colsum_rows": (i64, [i64]),
+    "dmt_bce_with_logits": (C.c_int, [vp, vp, i64, i32, f32, vp, vp, vp]),
     "dmt_column_sum_parts": (C.c_int, [vp, i64, i64, vp, vp]),
     "dmt_cross_bwd_pointwise": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, vp]),
     "dmt_sgd_dense": (C.c_int, [vp, vp, i64, f32, i32, vp]),

@@ -239,6 +239,29 @@ int convert_to(const void* src, void* dst, int32_t dto, int64_t n, cudaStream_t 
   return DMT_OK;
 }
 
+// Binary cross-entropy on logits, one block (deterministic loss sum):
+//   dz[i] = scale * (sigmoid(z[i]) - y[i]),   loss = scale * sum_i bce(z[i], y[i])
+// bce(z, y) = max(z, 0) - z y + log1p(exp(-|z|))  (stable form).
+template <typename T>
+__global__ void bce_logits_kernel(const T* __restrict__ z, const float* __restrict__ y, int64_t n, float scale,
+                                  T* __restrict__ dz, float* __restrict__ loss) {
+  __shared__ double part[256];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double zi = to_d<T>(z[i]), yi = y[i];
+    const double sg = 1.0 / (1.0 + exp(-zi));
+    dz[i] = from_d<T>(scale * (sg - yi));
+    acc += fmax(zi, 0.0) - zi * yi + log1p(exp(-fabs(zi)));
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && loss) *loss = (float)(scale * part[0]);
+}
+
 }  // namespace dmt
 
 extern "C" {
@@ -383,6 +406,23 @@ int dmt_sgd_dense(void* w, const float* g, int64_t n, float lr, int32_t dtype, d
     case DMT_F32: dmt::sgd_dense_kernel<float><<<grid, 256, 0, s>>>((float*)w, g, n, lr); break;
     case DMT_BF16: dmt::sgd_dense_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)w, g, n, lr); break;
     case DMT_F64: dmt::sgd_dense_kernel<double><<<grid, 256, 0, s>>>((double*)w, g, n, lr); break;
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_bce_with_logits(const void* z, const float* y, int64_t n, int32_t dtype, float scale, void* dz,
+                        float* loss, dmt_stream_t stream) {
+  if (n < 0) return DMT_ERR_SHAPE;
+  if (n == 0) return DMT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case DMT_F32: dmt::bce_logits_kernel<float><<<1, 256, 0, s>>>((const float*)z, y, n, scale, (float*)dz, loss); break;
+    case DMT_BF16:
+      dmt::bce_logits_kernel<__nv_bfloat16><<<1, 256, 0, s>>>((const __nv_bfloat16*)z, y, n, scale,
+                                                              (__nv_bfloat16*)dz, loss);
+      break;
     default: return DMT_ERR_UNSUPPORTED;
   }
   DMT_CHECK_LAUNCH();

@@ -392,6 +392,21 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[
     return out
 
 
+def bce_with_logits(z: torch.Tensor, y: torch.Tensor, scale: float, dz: Optional[torch.Tensor] = None,
+                    loss: Optional[torch.Tensor] = None):
+    """dz = scale (sigmoid(z) - y); loss[0] = scale * sum BCE(z, y) (fp32)."""
+    n = z.numel()
+    if y.numel() != n:
+        raise ShapeError(f"labels {tuple(y.shape)} do not match logits {tuple(z.shape)}")
+    if dz is None:
+        dz = torch.empty_like(z)
+    if loss is None:
+        loss = torch.empty(1, dtype=torch.float32, device=z.device)
+    L.check(L.lib().dmt_bce_with_logits(z.data_ptr(), y.data_ptr(), n, _dt(z), float(scale), dz.data_ptr(),
+                                        loss.data_ptr(), L.stream_ptr()), "dmt_bce_with_logits")
+    return dz, loss
+
+
 def colsum_rows(m: int) -> int:
     return int(L.lib().dmt_gemm_colsum_rows(m))
 

@@ -537,6 +537,8 @@ class SpttEngine:
                 fab.all_reduce_(group, grads)
                 self.tm[t].grads = grads
                 self.tm[t].sgd_step(tm_lr if tm_lr is not None else lr)
+            if dense_hook is not None:  # data-parallel layers above SPTT (world all-reduce + SGD)
+                dense_hook()
 
         self.overlap_with_embedding_update(tm_reduce_and_step, lr, optimizer, eps)
 

@@ -17,6 +17,8 @@ import numpy as np
 import torch
 
 from . import _lib as L
+from . import kernels as K
+from .errors import DomainError
 from .embedding import EmbeddingTable, ShardedEmbedding, TablePlan, shard_tables
 from .fabric import Fabric, LoopbackFabric
 from .pipeline import KJT, SpttEngine
@@ -30,7 +32,7 @@ class SPTT:
                  feature_towers: dict, pooling: dict, local_batch: int, fabric: Fabric,
                  tm: Optional[object] = None, dtype: torch.dtype = torch.float32, device=None,
                  mode: str = "sptt", lr: float = 0.01, optimizer: str = "sgd", eps: float = 1e-8,
-                 trace=None):
+                 trace=None, top: Optional[TMConfig] = None):
         self.topo, self.layout, self.placement = topo, layout, placement
         self.device = device or torch.device("cuda")
         feats = sorted(pooling)
@@ -64,6 +66,18 @@ class SPTT:
             n = ds.pop()
             self.global_tm = TowerModule(tm, len(feats), n, init_tm_weights(tm, len(feats), n, salt=0),
                                          dtype=dtype, device=self.device)
+        # dense head above the exchange (data parallel, replicated on every
+        # rank): the full DCN + SPTT model's top crossnet + logit projection,
+        # a TowerModule over one "feature" of the whole SPTT output width
+        self.top = None
+        if top is not None:
+            w_in = self.out_width
+            if top.kind == PASSTHROUGH or tm_output_width(top, 1, w_in) != 1:
+                raise DomainError("the top model must project to one logit (dcn out_dim=1 / dlrm c=1, p=0, "
+                                  "out_dim=1)")
+            self.top = TowerModule(top, 1, w_in, init_tm_weights(top, 1, w_in, salt=1_000_003), dtype=dtype,
+                                   device=self.device)
+            self._labels_loss = {}
         self.lr, self.eps = lr, eps
         self.opt = L.OPT_ROWWISE_ADAGRAD if optimizer == "adagrad" else L.OPT_SGD
         if self.opt == L.OPT_ROWWISE_ADAGRAD:
@@ -87,9 +101,9 @@ class SPTT:
             self._gsaved[r] = self.global_tm._saved
         return ys
 
-    def backward(self, grads: dict) -> None:
+    def backward(self, grads: dict, dense_hook=None) -> None:
         if self.global_tm is None:
-            self.engine.backward(grads, self.lr, self.opt, self.eps)
+            self.engine.backward(grads, self.lr, self.opt, self.eps, dense_hook=dense_hook)
             return
         dx, acc = {}, {}
         for r, g in grads.items():
@@ -103,6 +117,8 @@ class SPTT:
             self.fabric.all_reduce_(list(range(self.plan.G)), acc)
             self.global_tm.grads = acc
             self.global_tm.sgd_step(self.lr)
+            if dense_hook is not None:
+                dense_hook()
 
         self.engine.backward(dx, self.lr, self.opt, self.eps, dense_hook=dense_step)
 
@@ -111,7 +127,40 @@ class SPTT:
         self.backward(grads)
         return outs
 
-    def capture(self, kjts: dict, grads: dict, warmup: int = 2, timers=None):
+    def train_step_bce(self, kjts: dict, labels: dict) -> dict:
+        """Full model step with a loss: SPTT forward, top head -> logit, binary
+        cross-entropy against ``labels[r]`` (B,) fp32 (mean over the global
+        batch), top backward, SPTT backward with the top's gradient all-reduce
+        + SGD overlapped with the embedding update.  Returns {rank: loss (1,)}
+        (rank r's share of the global mean loss)."""
+        if self.top is None:
+            raise DomainError("train_step_bce needs SPTT(top=...)")
+        outs = self.forward(kjts, save=True)
+        scale = 1.0 / (self.plan.G * self.plan.B)
+        saved, gx, losses, acc = {}, {}, {}, {}
+        for r, o in outs.items():
+            with self.engine._t("top_fwd"):
+                z = self.top.forward(o, save=True)
+            buf = self._labels_loss.get(r)
+            if buf is None:
+                buf = self._labels_loss[r] = (torch.empty_like(z), torch.zeros(1, dtype=torch.float32,
+                                                                               device=self.device))
+            K.bce_with_logits(z, labels[r], scale, dz=buf[0], loss=buf[1])
+            losses[r] = buf[1]
+            with self.engine._t("top_bwd"):
+                gx[r] = self.top.backward(buf[0])
+            for k, v in self.top.grads.items():
+                acc[k] = v.clone() if k not in acc else acc[k].add_(v)
+
+        def top_step():  # world all-reduce of the head's grads + SGD
+            self.fabric.all_reduce_(list(range(self.plan.G)), acc)
+            self.top.grads = acc
+            self.top.sgd_step(self.lr)
+
+        self.backward(gx, dense_hook=top_step)
+        return losses
+
+    def capture(self, kjts: dict, grads: Optional[dict], warmup: int = 2, timers=None, labels: Optional[dict] = None):
         """Capture one full train step (forward a-f, backward, optimizer
         updates) as a CUDA graph over the given static input buffers.
 
@@ -124,16 +173,18 @@ class SPTT:
         self.engine.uniform_nnz = True
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
+        step = (lambda: self.train_step_bce(kjts, labels)) if labels is not None else (
+            lambda: self.train_step(kjts, grads))
         with torch.cuda.stream(s):
             for _ in range(warmup):
-                self.train_step(kjts, grads)
+                step()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         self.engine.timers = timers  # external events -> graph nodes
         try:
             with torch.cuda.graph(graph):
-                outs = self.train_step(kjts, grads)
+                outs = step()
         finally:
             self.engine.timers = None
         return graph.replay, outs

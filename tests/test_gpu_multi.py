@@ -66,14 +66,17 @@ def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1):
         Fab = PeerFabric if kind == "peer" else NcclFabric
         fab = Fab(world, rank, layout.group_width(topo), dev)
         dist_model = SPTT(topo, layout, placement, assignment, pooling, B, fab, tm=cfg, dtype=torch.float32,
-                          device=dev, lr=0.05)
+                          device=dev, lr=0.005)
         # reference: every rank on this GPU through the loopback fabric
         topo2, layout2, placement2, _, _, _, kjts2, _ = _build(hosts, rph, dev)
         ref = SPTT(topo2, layout2, placement2, assignment, pooling, B, LoopbackFabric(world, dev), tm=cfg,
-                   dtype=torch.float32, device=dev, lr=0.05)
+                   dtype=torch.float32, device=dev, lr=0.005)
         gen = np.random.default_rng(5)
         O = dist_model.plan.out_width()
         grads = {r: torch.from_numpy(gen.normal(size=(B, O)).astype(np.float32)).to(dev) for r in range(world)}
+        # lr is small: at W = 4 every tower module sees 4B rows and lr 0.05
+        # drives the DCN (quadratic in x) into divergence by step 3 -- two
+        # diverging trajectories cannot be compared (tools/debug_peer.py).
         # The tower all-reduce of the TM weight gradients sums W contributions
         # in NCCL's ring order; the loopback engine sums them in rank order.
         # For W <= 2 the two agree bit for bit (fp add commutes); for W > 2 the

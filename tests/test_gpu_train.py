@@ -247,3 +247,97 @@ def test_dcn_fused_sgd_matches_unfused(dt):
     assert torch.allclose(dxa.double(), dxb.double(), rtol=tol, atol=tol)
     for k in tm_a.w:
         assert torch.allclose(tm_a.w[k].double(), tm_b.w[k].double(), rtol=tol, atol=tol), k
+
+
+@pytest.mark.parametrize("hosts,rph,top_kind", [(2, 2, "dcn"), (1, 2, "dlrm"), (2, 1, "dcn")])
+def test_full_model_bce_step_loopback_vs_oracle(hosts, rph, top_kind):
+    """DCN + SPTT model with a loss: SPTT (DCN tower modules) -> top head
+    (crossnet + one-logit projection, or a one-logit linear) -> BCE on labels.
+    Loss, top weights after SGD and every embedding row after SGD vs the
+    oracle's flat-model restatement (fp32, rtol 1e-4)."""
+    import paper_2403_00877_b200 as P
+    from paper_2403_00877_b200.fabric import LoopbackFabric
+    from paper_2403_00877_b200.pipeline import KJT
+    from paper_2403_00877_b200.sptt import SPTT, build_world
+
+    F, rows, N, B = 6, 50, 16, 4
+    topo, layout, placement, assignment = build_world(hosts, rph, 1, F, rows, N, seed=3)
+    G, T = topo.world_size, layout.num_towers
+    pooling = {f: "sum" for f in range(F)}
+    cfg = P.TMConfig(kind="dcn", out_dim=4, cross_layers=2, seed=1)
+    ocfg = {"kind": "dcn", "out_dim": 4, "per_feature_outputs": 1, "flat_outputs": 0, "cross_layers": 2, "seed": 1}
+    if top_kind == "dcn":
+        top = P.TMConfig(kind="dcn", out_dim=1, cross_layers=2, seed=7)
+        otop = {"kind": "dcn", "out_dim": 1, "per_feature_outputs": 1, "flat_outputs": 0, "cross_layers": 2,
+                "seed": 7}
+    else:
+        top = P.TMConfig(kind="dlrm", out_dim=1, per_feature_outputs=1, flat_outputs=0, seed=7)
+        otop = {"kind": "dlrm", "out_dim": 1, "per_feature_outputs": 1, "flat_outputs": 0, "cross_layers": 3,
+                "seed": 7}
+    before = {t: placement.tables[t].values.astype(np.float64).copy() for t in range(F)}
+    lr = 0.1
+    model = SPTT(topo, layout, placement, assignment, pooling, B, LoopbackFabric(G, dev()), tm=cfg,
+                 dtype=torch.float32, lr=lr, top=top)
+    rng = np.random.default_rng(5)
+    lens = rng.integers(1, 4, size=(G, F, B)).astype(np.int32)
+    vals = rng.integers(0, rows, size=int(lens.sum())).astype(np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens.reshape(-1))])
+    kjts, labels = {}, {}
+    yl = rng.integers(0, 2, size=(G, B)).astype(np.float32)
+    for r in range(G):
+        seg = vals[offs[r * F * B]:offs[(r + 1) * F * B]]
+        kjts[r] = KJT(torch.from_numpy(lens[r].reshape(-1)).to(dev()), torch.from_numpy(seg.astype(np.int32)).to(dev()),
+                      [int(lens[r, f].sum()) for f in range(F)], B)
+        labels[r] = torch.from_numpy(yl[r]).to(dev())
+    top_w0 = model.top.host_weights()
+    losses = model.train_step_bce(kjts, labels)
+    torch.cuda.synchronize()
+
+    shards = [(s.table_id, s.rank, s.scheme, s.row_range, s.col_range) for s in placement.shards]
+    flat, _, _, _ = oracle.baseline_forward(lens, vals, list(range(F)), pooling, before, shards,
+                                            oracle.OTopo(hosts, rph))
+    by_tower = {t: [f for f in range(F) if assignment[f] == t] for t in range(T)}
+    tw = {t: oracle.init_tm_weights(ocfg, len(by_tower[t]), N, salt=t) for t in range(T)}
+    O = model.plan.out_width()
+    otw = oracle.init_tm_weights(otop, 1, O, salt=1_000_003)
+    np.testing.assert_allclose(top_w0.w_proj if top_kind == "dcn" else top_w0.w_feat,
+                               otw.w_proj if top_kind == "dcn" else otw.w_feat, rtol=1e-6)
+    grad_rows = {t: np.zeros_like(before[t]) for t in range(F)}
+    scale = 1.0 / (G * B)
+    top_grad_sum = None
+    for r in range(G):
+        col, ys, xs = 0, [], {}
+        for t in range(T):
+            fs = by_tower[t]
+            xs[t] = flat[r][:, fs[0] * N:(fs[-1] + 1) * N].reshape(B, len(fs), N)
+            ys.append(oracle.tm_forward(xs[t], ocfg, tw[t]))
+        y = np.concatenate(ys, axis=1)
+        z = oracle.tm_forward(y.reshape(B, 1, O), otop, otw)
+        loss, dz = oracle.bce_with_logits(z, yl[r].reshape(B, 1), scale)
+        assert abs(float(losses[r].item()) - loss) <= 1e-5 * max(1.0, abs(loss))
+        gy, gw = oracle.tm_backward(y.reshape(B, 1, O), otop, otw, dz)
+        gy = gy.reshape(B, O)
+        leaf = (lambda w: w.w_proj) if top_kind == "dcn" else (lambda w: w.w_feat)
+        top_grad_sum = leaf(gw) if top_grad_sum is None else top_grad_sum + leaf(gw)
+        for t in range(T):
+            fs = by_tower[t]
+            ow_ = oracle.tm_output_width(ocfg, len(fs), N)
+            dx, _ = oracle.tm_backward(xs[t], ocfg, tw[t], gy[:, col:col + ow_])
+            col += ow_
+            for i, f in enumerate(fs):
+                base = (r * F + f) * B
+                for b in range(B):
+                    for k in range(offs[base + b], offs[base + b + 1]):
+                        grad_rows[f][vals[k]] += dx[b, i]
+    wt = model.top.host_weights()
+    got_leaf = wt.w_proj if top_kind == "dcn" else wt.w_feat
+    want_leaf = (otw.w_proj if top_kind == "dcn" else otw.w_feat) - lr * top_grad_sum
+    np.testing.assert_allclose(got_leaf, want_leaf, rtol=1e-4, atol=1e-6)
+    for sid, sh in enumerate(placement.shards):
+        f = sh.table_id
+        touched = np.unique(vals[np.concatenate([np.arange(offs[(r * F + f) * B], offs[(r * F + f + 1) * B])
+                                                 for r in range(G)])])
+        want = oracle.apply_sgd(before[f], touched, grad_rows[f][touched], lr)
+        got = model.engine.weights[sid].double().cpu().numpy()
+        (r0, r1), (c0, c1) = sh.row_range, sh.col_range
+        np.testing.assert_allclose(got, want[r0:r1, c0:c1], rtol=1e-4, atol=1e-6)

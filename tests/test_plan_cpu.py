@@ -166,3 +166,31 @@ def test_product_refuses_cpu_fallback(monkeypatch):
     monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
     with pytest.raises(P.TowersimError):
         _lib.lib()
+
+
+@pytest.mark.parametrize("i", range(N_ACC))
+def test_plan_trace_matches_reference_trace(i):
+    """costmodel.plan_trace (host-side bytes from the plan, no run) equals the
+    reference's recorded sent_by_rank per step at its 4 B/element wire format:
+    step a, c (flat), d (all-to-all form), f (pass-through towers)."""
+    from paper_2403_00877_b200 import costmodel as cm
+
+    c = acceptance_case(i)
+    m = c["meta"]
+    lengths = c["lengths"]  # (G, F, B)
+    nnz = {r: [int(lengths[r, j].sum()) for j in range(lengths.shape[1])] for r in range(lengths.shape[0])}
+    tower = cm.plan_trace(_plan(c), nnz, 4, "sptt")
+    flat = cm.plan_trace(_plan(c, sptt=False), nnz, 4, "flat")
+    rs = m["cfg"]["exchange"]["rowwise_reducescatter"]
+    has_tm = float(m["flops"].get("e", 0.0)) > 0
+    want_t, want_b = m["tower_trace"], m["base_trace"]
+
+    def sent(tr, label):
+        return {str(k): v for k, v in tr.sent_by_rank(label).items()}
+
+    assert sent(flat, "a") == want_b["a_sent"] and sent(flat, "c") == want_b["c_sent"]
+    assert sent(tower, "a") == want_t["a_sent"]
+    if not rs:
+        assert sent(tower, "d") == want_t["d_sent"]
+    if not has_tm:
+        assert sent(tower, "f") == want_t["f_sent"]
