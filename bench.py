@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--rows", type=int, default=1_000_000)
     ap.add_argument("--dim", type=int, default=128)
     ap.add_argument("--pool", type=int, default=20)
+    ap.add_argument("--pool-dist", default="fixed", choices=["fixed", "powerlaw"],
+                    help="fixed L = --pool (C2/C3), or power-law lengths with mean --pool, max 200 (C5; ragged "
+                         "nnz -> eager steps, no CUDA graph)")
     ap.add_argument("--batch", type=int, default=8192)
     ap.add_argument("--tm", default="dcn", choices=["dcn", "dlrm", "passthrough"])
     ap.add_argument("--tm-out", type=int, default=64)
@@ -192,12 +195,18 @@ def cpu_baseline(args) -> dict:
 
 def _config(args, N):
     T = _towers(args, N)
-    return {"workload": "C2 (BASELINE configs[1]): 26 tables x 1M rows x dim 128, pooling 20, batch 8192/GPU, "
-                        f"{args.tm} TM" if N == 1 else
-                        f"C2 per GPU, SPTT {T} towers x {N // T} GPUs, flat all-to-all alongside",
+    if args.pool_dist == "powerlaw":
+        wl = (f"C5-style: {args.tables} tables x {args.rows} rows x dim {args.dim}, power-law pooling (mean "
+              f"{args.pool}, max 200), batch {args.batch}/GPU, {args.tm} TM, SPTT {T} x {N // T}")
+    elif N == 1:
+        wl = f"C2 (BASELINE configs[1]): 26 tables x 1M rows x dim 128, pooling 20, batch 8192/GPU, {args.tm} TM"
+    else:
+        wl = f"C2 per GPU, SPTT {T} towers x {N // T} GPUs, flat all-to-all alongside"
+    return {"workload": wl,
             "tables": args.tables, "rows": args.rows, "dim": args.dim, "pooling_factor": args.pool,
             "batch_per_gpu": args.batch, "global_batch": args.batch * N, "tm": args.tm, "tm_out_dim": args.tm_out,
             "cross_layers": args.cross_layers, "top": args.top, "towers": T, "gpus_per_tower": N // T, "optimizer": "sgd",
+            "pooling_dist": args.pool_dist,
             "parallelism": f"embedding model-parallel in tower, TM data-parallel in tower (T={T}, W={N // T})",
             "exchange": "loopback" if N == 1 else ("nvlink peer stores + barrier" if args.fabric == "peer"
                                                    else "nccl all-to-all"),
@@ -278,7 +287,13 @@ def main():
     model = SPTT(topo, layout, placement, assignment, pooling, B, fabric, tm=tm_cfg, dtype=dtype, device=dev,
                  mode="sptt", lr=1e-3, top=top_cfg)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    batches = [{rank: random_kjt(F, B, args.rows, Lp, gen, dev)} for _ in range(4)]
+    if args.pool_dist == "powerlaw":
+        from paper_2403_00877_b200.sptt import powerlaw_lengths, random_kjt_lengths
+
+        batches = [{rank: random_kjt_lengths(powerlaw_lengths(F, B, 100 * i + rank, mean=float(Lp)), args.rows, gen,
+                                             dev)} for i in range(4)]
+    else:
+        batches = [{rank: random_kjt(F, B, args.rows, Lp, gen, dev)} for _ in range(4)]
     gout = {rank: (torch.randn(B, model.out_width, generator=gen, device=dev) * 1e-3).to(dtype)}
     labels = {rank: (torch.rand(B, generator=gen, device=dev) < 0.25).float()}  # synthetic CTR labels
 
@@ -309,6 +324,28 @@ def main():
         barrier()
         m.engine.timers = None
         return s.elapsed_time(e), timers, (_lib.CALLS[0] - calls0) // max(K, 1)
+
+    def timed_eager_h2d(m, hosts, K):
+        """e2e without a CUDA graph (ragged batches): every step copies its
+        pinned host KJT to the device, runs the step and reads a scalar back."""
+        from paper_2403_00877_b200.pipeline import KJT as _KJT
+
+        out = torch.zeros(1, dtype=torch.float32).pin_memory()
+        for i in range(2):
+            hl, hv, nz = hosts[i % len(hosts)]
+            step(m, {rank: _KJT(hl.to(dev, non_blocking=True), hv.to(dev, non_blocking=True), nz, B)})
+        torch.cuda.synchronize()
+        barrier()
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record()
+        for i in range(K):
+            hl, hv, nz = hosts[i % len(hosts)]
+            o = step(m, {rank: _KJT(hl.to(dev, non_blocking=True), hv.to(dev, non_blocking=True), nz, B)})
+            out.copy_(o[rank].reshape(-1)[:1].float(), non_blocking=True)
+        e_.record()
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(s_.elapsed_time(e_))
 
     def max_over_ranks(ms):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -392,6 +429,8 @@ def main():
     clocks.start()
     gtimers = PhaseTimers(external=True)
     try:
+        if args.pool_dist != "fixed":
+            raise RuntimeError("ragged per-batch nnz: eager steps (step-a counts exchange per batch)")
         total_ms = timed_graph(model, args.steps, timers=gtimers)
         # phases of the last replay (events are graph nodes, re-recorded each replay)
         ph = {k: v for k, v in gtimers.ms().items()}
@@ -413,8 +452,8 @@ def main():
             hosts.append((kj.lengths.cpu().pin_memory(), kj.values.cpu().pin_memory(), kj.nnz_per_feature))
         if graph_ok:
             e_ms = timed_graph(model, args.steps, host_inputs=hosts)
-        else:
-            e_ms = max_over_ranks(eager_ms)
+        else:  # eager: H2D of each step's KJT from pinned host memory inside the region
+            e_ms = timed_eager_h2d(model, hosts, args.steps)
         h2d = hosts[0][0].numel() * 4 + hosts[0][1].numel() * 4
         e2e = {"value": N * B * args.steps / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 4}
@@ -422,7 +461,7 @@ def main():
     # roofline of the lookup kernel: algorithmic bytes per launch
     p = model.plan
     bags = p.owner_bags(rank)
-    nnz = bags * Lp
+    nnz = model.engine._owner[rank][2] if args.pool_dist != "fixed" else bags * Lp
     look_bytes = nnz * Nd * es + nnz * 4 + (bags + 1) * 8 + bags * Nd * es
     import json as _j
 

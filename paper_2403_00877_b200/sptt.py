@@ -265,6 +265,27 @@ def random_kjt(F: int, B: int, rows: int, L_: int, gen: torch.Generator, device)
     return KJT(lengths=lengths, values=values, nnz_per_feature=[B * L_] * F, B=B)
 
 
+def powerlaw_lengths(F: int, B: int, seed: int, mean: float = 20.0, cap: int = 200, alpha: float = 2.0) -> np.ndarray:
+    """C5 pooling factors: a seeded Pareto(alpha) with scale
+    chosen for the requested mean, truncated at ``cap`` and floored at 1,
+    (F, B) int32.  The reference's make_batch only draws uniform [lo, hi]
+    lengths (embedding.py:259-295); this builds the batch directly."""
+    rng = np.random.default_rng(seed)
+    xm = mean * (alpha - 1.0) / alpha
+    x = xm * (1.0 - rng.random((F, B))) ** (-1.0 / alpha)
+    return np.clip(np.floor(x), 1, cap).astype(np.int32)
+
+
+def random_kjt_lengths(lengths: np.ndarray, rows: int, gen: torch.Generator, device) -> KJT:
+    """KJT with the given (F, B) lengths and uniform indices in [0, rows);
+    per-feature nnz known on the host (no device sync for step-a splits)."""
+    F, B = lengths.shape
+    nnz = [int(x) for x in lengths.sum(axis=1)]
+    lens = torch.from_numpy(lengths.reshape(-1).copy()).to(device)
+    values = torch.randint(0, rows, (max(1, sum(nnz)),), generator=gen, device=device, dtype=torch.int32)[:sum(nnz)]
+    return KJT(lengths=lens, values=values, nnz_per_feature=nnz, B=B)
+
+
 def smoke_train_step() -> None:
     """One loopback SPTT train step (2 towers x 2 ranks, DLRM TM, fp32) checked
     against the oracle's flat-model restatement (used by __graft_entry__.smoke)."""

@@ -300,8 +300,8 @@ def test_full_model_bce_step_loopback_vs_oracle(hosts, rph, top_kind):
     tw = {t: oracle.init_tm_weights(ocfg, len(by_tower[t]), N, salt=t) for t in range(T)}
     O = model.plan.out_width()
     otw = oracle.init_tm_weights(otop, 1, O, salt=1_000_003)
-    np.testing.assert_allclose(top_w0.w_proj if top_kind == "dcn" else top_w0.w_feat,
-                               otw.w_proj if top_kind == "dcn" else otw.w_feat, rtol=1e-6)
+    key = "w_proj" if top_kind == "dcn" else "w_feat"
+    np.testing.assert_allclose(getattr(top_w0, key), otw[key], rtol=1e-6)
     grad_rows = {t: np.zeros_like(before[t]) for t in range(F)}
     scale = 1.0 / (G * B)
     top_grad_sum = None
@@ -317,8 +317,7 @@ def test_full_model_bce_step_loopback_vs_oracle(hosts, rph, top_kind):
         assert abs(float(losses[r].item()) - loss) <= 1e-5 * max(1.0, abs(loss))
         gy, gw = oracle.tm_backward(y.reshape(B, 1, O), otop, otw, dz)
         gy = gy.reshape(B, O)
-        leaf = (lambda w: w.w_proj) if top_kind == "dcn" else (lambda w: w.w_feat)
-        top_grad_sum = leaf(gw) if top_grad_sum is None else top_grad_sum + leaf(gw)
+        top_grad_sum = gw[key] if top_grad_sum is None else top_grad_sum + gw[key]
         for t in range(T):
             fs = by_tower[t]
             ow_ = oracle.tm_output_width(ocfg, len(fs), N)
@@ -330,8 +329,8 @@ def test_full_model_bce_step_loopback_vs_oracle(hosts, rph, top_kind):
                     for k in range(offs[base + b], offs[base + b + 1]):
                         grad_rows[f][vals[k]] += dx[b, i]
     wt = model.top.host_weights()
-    got_leaf = wt.w_proj if top_kind == "dcn" else wt.w_feat
-    want_leaf = (otw.w_proj if top_kind == "dcn" else otw.w_feat) - lr * top_grad_sum
+    got_leaf = getattr(wt, key)
+    want_leaf = otw[key] - lr * top_grad_sum
     np.testing.assert_allclose(got_leaf, want_leaf, rtol=1e-4, atol=1e-6)
     for sid, sh in enumerate(placement.shards):
         f = sh.table_id

@@ -194,3 +194,15 @@ def test_plan_trace_matches_reference_trace(i):
         assert sent(tower, "d") == want_t["d_sent"]
     if not has_tm:
         assert sent(tower, "f") == want_t["f_sent"]
+
+
+def test_powerlaw_lengths_c5():
+    """C5 pooling factors: seeded, in [1, 200], mean ~ 20, heavy tail."""
+    from paper_2403_00877_b200.sptt import powerlaw_lengths
+
+    a = powerlaw_lengths(512, 4096, seed=3)
+    b = powerlaw_lengths(512, 4096, seed=3)
+    assert np.array_equal(a, b) and a.dtype == np.int32 and a.shape == (512, 4096)
+    assert a.min() >= 1 and a.max() <= 200
+    assert 15.0 < a.mean() < 22.0
+    assert (a >= 100).mean() > 0.005  # heavy tail present
