@@ -234,6 +234,8 @@ enum dmt_gemm_flags {
   /* tuning overrides (benchmarks): no L2 prefetch of the epilogue operands;
    * force the tile width BN = 64 * ((flags & BN_MASK) >> BN_SHIFT) */
   DMT_GEMM_NO_PREFETCH = 16,
+  /* opt-in: 2-CTA clusters sharing each B tile (TMA multicast) */
+  DMT_GEMM_CLUSTER = 32,
   DMT_GEMM_BN_SHIFT = 8,
   DMT_GEMM_BN_MASK = 0xF00
 };

@@ -76,6 +76,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// TMA load delivered to the same shared-memory offset of every CTA in
+// ``mask`` (cluster multicast), completing tx bytes on each one's mbarrier.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -93,6 +112,14 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t b
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
   }
+}
+
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -150,6 +177,21 @@ struct Operand {
   }
   __device__ static __forceinline__ uint64_t kstep(int kk) {
     return MN ? (uint64_t)(((uint32_t)kk * (4096u / ES)) >> 4) : (uint64_t)((kk * kUmmaKBytes) >> 4);
+  }
+  // CTA ``rank`` of a 2-CTA cluster loads its share of a ROWS-row tile and
+  // multicasts it to both: K-major -> row half [rank*ROWS/2, +ROWS/2) (the
+  // map's box has ROWS/2 rows); MN-major -> the 128-byte MN atoms c with
+  // c % 2 == rank.
+  template <int ROWS>
+  __device__ static __forceinline__ void load_half_mc(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0,
+                                                      int r0, int rank) {
+    if constexpr (!MN) {
+      tma_load_2d_mc(dst + rank * (ROWS / 2) * kAtomBytes, map, bar, k0, r0 + rank * (ROWS / 2), 0x3);
+    } else {
+#pragma unroll
+      for (int c = 0; c < ROWS / ATOM; ++c)
+        if ((c & 1) == rank) tma_load_2d_mc(dst + c * COL_BYTES, map, bar, r0 + c * ATOM, k0, 0x3);
+    }
   }
   template <int ROWS>
   __device__ static __forceinline__ void load(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0, int r0) {
@@ -474,7 +516,10 @@ __device__ __forceinline__ void colsum_chunk(const Params& p, float* stile, int6
 // BN: tile N (64/128/256); NOPS: 1 (plain) or 3 (3xTF32); KIND: 0 f16-family, 1 tf32
 // FEAT: compile in the DCN-backward extras (fused bias-gradient column sums,
 // DCN_FINAL pair sums); kept out of the other variants' register budget.
-template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN, bool FEAT>
+// CL: CTAs per cluster along M (1, or 2 = the pair shares each B tile: both
+// CTAs load half and multicast it, halving B's L2 -> SM traffic).
+template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN, bool FEAT,
+          int CL = 1>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_lo,
@@ -496,7 +541,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tiles_m = ceil_div(p.m, kBlockM), tiles_n = ceil_div(p.n, BN);
-  const int64_t num_tiles = tiles_m * tiles_n;
+  // work unit = CL vertically adjacent tiles sharing n0 (one per cluster CTA)
+  const int64_t num_units = (tiles_m / CL) * tiles_n;
+  const int crank = CL > 1 ? (int)cluster_rank() : 0;
+  const int64_t u_first = blockIdx.x / CL, u_step = gridDim.x / CL;
+  auto unit_m0 = [&](int64_t u) { return (int64_t)(((u / tiles_n) * CL + crank) * kBlockM); };
+  auto unit_n0 = [&](int64_t u) { return (int64_t)((u % tiles_n) * BN); };
   const int num_kb = (int)ceil_div(p.k * (int64_t)sizeof(TIN), kAtomBytes);
   constexpr int K_ELEMS = kAtomBytes / sizeof(TIN);
   using OA = Operand<TIN, AMN>;
@@ -505,7 +555,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // released by every cluster CTA's MMA warp
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -520,7 +570,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -532,9 +583,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     }
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (int)((tile / tiles_n) * kBlockM);
-      const int n0 = (int)((tile % tiles_n) * BN);
+    for (int64_t u = u_first; u < num_units; u += u_step) {
+      const int m0 = (int)unit_m0(u);
+      const int n0 = (int)unit_n0(u);
       if (lane == 0 && p.prefetch) {
         if (p.prefetch & 1) l2_prefetch_2d(&emaps.x0, n0, m0);
         if (p.prefetch & 2) l2_prefetch_2d(&emaps.xl, n0, m0);
@@ -548,7 +599,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           uint8_t* sb = sa + A_BYTES;
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           OA::template load<kBlockM>(sa, &map_a, &full[stage], kb * K_ELEMS, m0);
-          OB::template load<BN>(sb, &map_b, &full[stage], kb * K_ELEMS, n0);
+          if constexpr (CL > 1) OB::template load_half_mc<BN>(sb, &map_b, &full[stage], kb * K_ELEMS, n0, crank);
+          else OB::template load<BN>(sb, &map_b, &full[stage], kb * K_ELEMS, n0);
           if constexpr (NSETS == 2) {
             uint8_t* sa2 = sb + B_BYTES;
             uint8_t* sb2 = sa2 + A_BYTES;
@@ -566,7 +618,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int64_t u = u_first; u < num_units; u += u_step, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -593,7 +645,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
               umma<KIND>(tmem_d, da2 + ada, db + adb, idesc, 1u);  // lo * hi
             }
           }
-          umma_commit(&empty[stage]);  // smem slot reusable once these MMAs retire
+          // smem slot reusable once these MMAs retire (in every cluster CTA:
+          // the peer multicasts into this slot too)
+          if constexpr (CL > 1) umma_commit_mc(&empty[stage], 0x3);
+          else umma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         umma_commit(&tfull[acc]);  // accumulator complete
@@ -605,11 +660,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     const int half = (warp - 2) / 4;              // which half of the tile's columns
     constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int64_t u = u_first; u < num_units; u += u_step, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int64_t m0 = (tile / tiles_n) * kBlockM;
-      const int64_t n0 = (tile % tiles_n) * BN;
+      const int64_t m0 = unit_m0(u);
+      const int64_t n0 = unit_n0(u);
       float* stile = stile_all + (warp - 2) * kStileFloats;
       if (p.coalesced && n0 + (int64_t)(half + 1) * kColsPerWarp <= p.n) {
         // Pipelined full-width path: the epilogue operands (x0 / u / C / dx0)
@@ -847,6 +902,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
   }
+  // no CTA may exit while its peer can still multicast into it / arrive on it
+  if constexpr (CL > 1) cluster_sync_all();
 }
 
 // ---------------------------------------------------------------- host ------
@@ -916,7 +973,8 @@ static bool make_plain_map(CUtensorMap* map, const void* ptr, int64_t rows, int6
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN, bool FEAT>
+template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN, bool FEAT,
+          int CL = 1>
 static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cudaStream_t s) {
   constexpr int NSETS = (NOPS == 3) ? 2 : 1;
   constexpr int STAGE_BYTES = NSETS * (kBlockM + BN) * kAtomBytes;
@@ -925,7 +983,9 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   static_assert(SMEM <= 232448, "smem");
   CUtensorMap ma, mb, mal, mbl;
   if (!make_map(&ma, a->a, a->m, a->k, a->lda, a->in_dtype, kBlockM, AMN)) return DMT_ERR_CUDA;
-  if (!make_map(&mb, a->b, a->n, a->k, a->ldb, a->in_dtype, BN, BMN)) return DMT_ERR_CUDA;
+  // 2-CTA clusters: a K-major B box covers the CTA's half of the tile rows
+  if (!make_map(&mb, a->b, a->n, a->k, a->ldb, a->in_dtype, (CL > 1 && !BMN) ? BN / CL : BN, BMN))
+    return DMT_ERR_CUDA;
   if (NSETS == 2) {
     if (!make_map(&mal, a_lo, a->m, a->k, a->lda, a->in_dtype, kBlockM, AMN)) return DMT_ERR_CUDA;
     if (!make_map(&mbl, b_lo, a->n, a->k, a->ldb, a->in_dtype, BN, BMN)) return DMT_ERR_CUDA;
@@ -987,7 +1047,7 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
     if (!ok) p.prefetch = 0;  // a hint only: skip it when a block cannot be described
   }
   if (a->bias && ((uintptr_t)a->bias % 16)) return DMT_ERR_UNSUPPORTED;
-  auto kern = gemm_kernel<BN, NOPS, KIND, STAGES, TIN, TO, AMN, BMN, FEAT>;
+  auto kern = gemm_kernel<BN, NOPS, KIND, STAGES, TIN, TO, AMN, BMN, FEAT, CL>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
@@ -998,10 +1058,40 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
     attr_set = true;
   }
   int64_t tiles = ceil_div(a->m, kBlockM) * ceil_div(a->n, BN);
-  int grid = (int)std::min<int64_t>(tiles, DMT_NUM_SMS);
   const int fmt = (KIND == 1) ? 2 : (std::is_same<TIN, __half>::value ? 0 : 1);
   uint32_t idesc = make_idesc(fmt, kBlockM, BN, AMN, BMN);
-  kern<<<grid, kThreads, SMEM, s>>>(ma, mb, mal, mbl, em, p, idesc);
+  if constexpr (CL == 1) {
+    int grid = (int)std::min<int64_t>(tiles, DMT_NUM_SMS);
+    kern<<<grid, kThreads, SMEM, s>>>(ma, mb, mal, mbl, em, p, idesc);
+  } else {
+    // persistent over co-resident clusters only (GPCs with an odd SM count
+    // cannot host a full pair on every SM)
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static int max_clusters = 0;
+    if (!max_clusters) {
+      cfg.gridDim = dim3(DMT_NUM_SMS / CL * CL);
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = DMT_NUM_SMS / CL;
+      max_clusters = n;
+    }
+    const int64_t units = tiles / CL;
+    cfg.gridDim = dim3((unsigned)(std::min<int64_t>(units, max_clusters) * CL));
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mal, mbl, em, p, idesc);
+    if (e != cudaSuccess) {
+      set_last_error(e);
+      return DMT_ERR_CUDA;
+    }
+  }
   DMT_CHECK_LAUNCH();
   return DMT_OK;
 }
@@ -1042,7 +1132,19 @@ static int dispatch_n(const dmt_gemm_args* a, const void* alo, const void* blo, 
     if (a->n <= 64) return launch<64, 3, 1, 4, TIN, TO, AMN, BMN, FEAT>(a, alo, blo, s);
     return launch<128, 3, 1, 3, TIN, TO, AMN, BMN, FEAT>(a, alo, blo, s);
   } else {
-    switch (pick_bn(a->m, a->n, a->flags)) {
+    const int bn = pick_bn(a->m, a->n, a->flags);
+    if constexpr (std::is_same<TIN, __nv_bfloat16>::value && !FEAT) {
+      // 2-CTA clusters sharing B (multicast), opt-in: parity-green, but it
+      // measured equal to the single-CTA kernel (the mainloop is not bound by
+      // L2 -> SM operand traffic), so the default stays single-CTA
+      const bool pair = (a->flags & DMT_GEMM_CLUSTER) && (ceil_div(a->m, kBlockM) % 2 == 0) &&
+                        (bn == 256 || bn == 192) && ceil_div(a->m, kBlockM) * ceil_div(a->n, (int64_t)bn) >= 2 * 148;
+      if (pair) {
+        if (bn == 256) return launch<256, 1, 0, 4, TIN, TO, AMN, BMN, FEAT, 2>(a, alo, blo, s);
+        return launch<192, 1, 0, 4, TIN, TO, AMN, BMN, FEAT, 2>(a, alo, blo, s);
+      }
+    }
+    switch (bn) {
       case 64: return launch<64, 1, 0, 8, TIN, TO, AMN, BMN, FEAT>(a, alo, blo, s);
       case 128: return launch<128, 1, 0, 6, TIN, TO, AMN, BMN, FEAT>(a, alo, blo, s);
       case 192: return launch<192, 1, 0, 4, TIN, TO, AMN, BMN, FEAT>(a, alo, blo, s);

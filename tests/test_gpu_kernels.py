@@ -212,3 +212,26 @@ def test_gemm_mn_major_operands(ta, tb, dt, m, n, k):
     tol = 1e-5 if dt == torch.float32 else 1e-2
     scale = (A.double().abs() @ Bm.double().abs().T).max().item()
     assert (out.double() - want).abs().max().item() <= tol * scale
+
+
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("m,n,k", [(8192, 1536, 256), (4096, 2560, 192)])
+def test_gemm_cluster_multicast_matches_single_cta(tb, m, n, k):
+    """Opt-in 2-CTA cluster variant (each CTA loads half of the B tile and
+    multicasts it): bit-identical to the single-CTA kernel (same MMA order)."""
+    from paper_2403_00877_b200 import _lib as L
+    from paper_2403_00877_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
+    Bm = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+    b = Bm.t().contiguous() if tb else Bm
+    bias = torch.randn(n, device="cuda", generator=g)
+    x0 = torch.randn(m, n, device="cuda", generator=g).to(torch.bfloat16)
+    outs = []
+    for fl in (0, L.GEMM_CLUSTER):
+        o = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+        K.gemm(A, b, o, trans_b=tb, bias=bias, epilogue=L.EPI_CROSS, x0=x0, xl=x0, tune_flags=fl)
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])

@@ -88,9 +88,9 @@ def main():
          lambda: K.gemm(gy, Wp, out, trans_b=True, epilogue=L.EPI_DCN_BWD, x0=x0, xl=u, aux=xl, aux2=dx0),
          lambda: torch.matmul(gy, Wp)),
     ]
-    variants = [("auto", 0), ("nopf", L.GEMM_NO_PREFETCH)] + [
+    variants = [("auto", 0), ("cl2", L.GEMM_CLUSTER), ("nopf", L.GEMM_NO_PREFETCH)] + [
         (f"bn{64 * j}", j << L.GEMM_BN_SHIFT) for j in (3, 4)] + [
-        (f"bn{64 * j}np", (j << L.GEMM_BN_SHIFT) | L.GEMM_NO_PREFETCH) for j in (3, 4)]
+        (f"bn{64 * j}cl", (j << L.GEMM_BN_SHIFT) | L.GEMM_CLUSTER) for j in (3, 4)]
     for name, flops, fn, ref in cases:
         line = f"{name:22s}"
         for vname, fl in variants:
