@@ -239,6 +239,17 @@ struct Params {
   float* colsum;  // DCN_BWD: per (128-row tile, 32-row quarter) column sums of the stored gu
 };
 
+// Output row address.  The grouped layout (per-feature DLRM projection rows
+// scattered into the tower output) needs a 64-bit division; plain GEMMs take
+// the multiply-only branch (ncu showed the division's I2F / MUFU.RCP sequence
+// among the epilogue's hottest instructions).
+template <typename TO>
+__device__ __forceinline__ TO* out_row(const Params& p, int64_t row) {
+  TO* d = reinterpret_cast<TO*>(p.d);
+  if (p.rows_per_group > p.m) return d + row * p.ld_d;
+  return d + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
+}
+
 // 32 consecutive elements of one row <-> 32 fp32 registers.  The vector forms
 // need 16-byte alignment; the scalar forms are predicated (tail / unaligned).
 template <typename TX>
@@ -361,7 +372,7 @@ __device__ __forceinline__ void epi8(const Params& p, int64_t row, int64_t col, 
       store8<float>(p.aux2 + xo, d);
     }
   }
-  TO* drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
+  TO* drow = out_row<TO>(p, row);
   store8<TO>(drow + col, v);
 }
 
@@ -479,7 +490,7 @@ __device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t
       }
     }
   }
-  TO* drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
+  TO* drow = out_row<TO>(p, row);
   store8<TO>(drow + col, v);
 }
 
@@ -739,7 +750,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       const bool row_ok = row < p.m;
       TO* drow = nullptr;
       if (row_ok)
-        drow = reinterpret_cast<TO*>(p.d) + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
+        drow = out_row<TO>(p, row);
 #pragma unroll 1
       for (int c = half * kColsPerWarp; c < (half + 1) * kColsPerWarp; c += 32) {
         float v[32];
