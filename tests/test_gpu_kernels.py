@@ -235,3 +235,20 @@ def test_gemm_cluster_multicast_matches_single_cta(tb, m, n, k):
         outs.append(o)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("rows,cols", [(8192, 3328), (1000, 256), (77, 64), (3, 8), (4096, 100)])
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
+def test_column_sum_vs_fp64(rows, cols, dt):
+    """Bias-gradient column sums (DCN backward): fp32 partials folded into
+    fp64 every 32 rows, fixed-order final reduction -- deterministic."""
+    from paper_2403_00877_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(rows + cols)
+    x = torch.randn(rows, cols, device="cuda", generator=g).to(dt)
+    got = K.column_sum(x)
+    again = K.column_sum(x)
+    want = x.double().sum(0)
+    torch.cuda.synchronize()
+    assert torch.equal(got, again)
+    assert (got.double() - want).abs().max().item() <= 1e-5 * (x.double().abs().sum(0).max().item() + 1)
