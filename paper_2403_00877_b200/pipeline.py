@@ -130,6 +130,7 @@ class SpttEngine:
         self.buf = {}
         self.seg_fwd, self.seg_bwd = {}, {}
         self.asm_e, self.asm_out, self.asm_c = {}, {}, {}
+        self.direct_x = {}
         sptt = mode == "sptt"
         for r in self.local:
             nsend = p.send_d_size(r) if sptt else p.send_c_size(r)
@@ -154,8 +155,19 @@ class SpttEngine:
                                torch.empty(max(1, sum(p.c_recv_splits(r))), dtype=dtype, device=dev))
                 b["out"] = torch.empty((p.B, p.flat_width()), dtype=dtype, device=dev)
             self.buf[r] = b
-            self.seg_fwd[r] = self._segments(r, b["send_x"])
-            self.seg_bwd[r] = self._segments(r, b["grad_x"], with_keys=True)
+            xmap = self._direct_x_map(r) if sptt else None
+            if xmap is not None:
+                # one-rank tower (W = 1): steps c, d and the step-e regroup are
+                # all identities up to layout, so the lookup pools straight into
+                # the TM input X and the embedding backward reads its gradient
+                # rows straight from dX (no assemble / scatter copies)
+                b["gX"] = torch.empty_like(b["X"])
+                self.direct_x[r] = xmap
+                self.seg_fwd[r] = self._segments(r, b["X"], xmap=xmap)
+                self.seg_bwd[r] = self._segments(r, b["gX"], with_keys=True, xmap=xmap)
+            else:
+                self.seg_fwd[r] = self._segments(r, b["send_x"])
+                self.seg_bwd[r] = self._segments(r, b["grad_x"], with_keys=True)
             if sptt:
                 self.asm_e[r] = self._assemble_table(p.e_blocks(r), b["recv_d"], b["X"], p.T * p.B)
                 blocks = [K.Block(col, w, [(b["recv_f"], off, w)]) for col, w, off in p.out_blocks_tower()]
@@ -235,7 +247,31 @@ class SpttEngine:
         return t
 
     # ----------------------------------------------------------- tables ----
-    def _segments(self, r: int, out: torch.Tensor, with_keys: bool = False) -> K.SegmentTable:
+    def _direct_x_map(self, r: int) -> Optional[dict]:
+        """{(src block p, shard k): (element offset in X, row stride)} when rank r
+        is a one-rank tower whose TM input X can take the lookup output directly
+        (no row-wise shard sums, every shard of r inside its tower), else None."""
+        p = self.plan
+        t = p.tower_of(r)
+        if p.W != 1 or t not in self.tm:
+            return None
+        xw = p.x_width(r)
+        where = {}
+        for fb in p.e_blocks(r):
+            if fb.rowwise:
+                return None
+            for pc in fb.pieces:
+                where[pc.sid] = fb.dst_col + pc.c0
+        xmap = {}
+        for (pp, k, off, w) in p.lookup_out_offsets(r, True):
+            sid = p.by_owner[r][k]
+            if sid not in where:
+                return None
+            xmap[(pp, k)] = (pp * p.B * xw + where[sid], xw)
+        return xmap
+
+    def _segments(self, r: int, out: torch.Tensor, with_keys: bool = False,
+                  xmap: Optional[dict] = None) -> K.SegmentTable:
         p = self.plan
         segs = []
         key_base, kb = {}, 0
@@ -245,6 +281,8 @@ class SpttEngine:
         self.key_space = getattr(self, "key_space", {})
         self.key_space[r] = kb
         for (pp, k, off, w) in p.lookup_out_offsets(r, self.mode == "sptt"):
+            if xmap is not None:
+                off, w = xmap[(pp, k)]
             sid = p.by_owner[r][k]
             sh = self.placement.shards[sid]
             pool = p.pooling[sh.table_id]
@@ -275,7 +313,10 @@ class SpttEngine:
                 if sid not in self.state:
                     self.state[sid] = torch.zeros(self.placement.shards[sid].rows, dtype=torch.float32,
                                                   device=self.device)
-            self.seg_bwd[r] = self._segments(r, self.buf[r]["grad_x"], with_keys=True)
+            if self.direct_x.get(r):
+                self.seg_bwd[r] = self._segments(r, self.buf[r]["gX"], with_keys=True, xmap=self.direct_x[r])
+            else:
+                self.seg_bwd[r] = self._segments(r, self.buf[r]["grad_x"], with_keys=True)
 
     # ---------------------------------------------------------- forward ----
     def forward(self, kjts: dict, save: bool = False, check_indices: bool = False) -> dict:
@@ -358,7 +399,8 @@ class SpttEngine:
                               {r: p.d_recv_splits(r) for r in g}, None)
         # step e: regroup + tower module
         for r in self.local:
-            self.asm_e[r].run()
+            if not self.direct_x.get(r):
+                self.asm_e[r].run()
             t = p.tower_of(r)
             if t in self.tm:
                 with self._t("tm_fwd"):
@@ -492,7 +534,8 @@ class SpttEngine:
                 # SGD into the dW GEMM epilogues
                 fused = (tm_lr if tm_lr is not None else lr) if p.W == 1 else None
                 with self._t("tm_bwd"):
-                    dX[r] = self.tm[t].backward(grecv[r], fused_lr=fused)
+                    dX[r] = self.tm[t].backward(grecv[r], fused_lr=fused,
+                                                dx_out=self.buf[r]["gX"] if self.direct_x.get(r) else None)
                 acc = tower_grads.setdefault(t, {})
                 for k, v in self.tm[t].grads.items():
                     acc[k] = v.clone() if k not in acc else acc[k].add_(v)
@@ -501,6 +544,8 @@ class SpttEngine:
         # d^-1: scatter dX columns back into the step-d receive layout
         dsend, drecv = {}, {}
         for r in self.local:
+            if self.direct_x.get(r):
+                continue  # the embedding backward reads gX directly
             if self.p2p_d:
                 # d^-1 over NVLink: scatter dX columns straight into every
                 # owner's gradient buffer (its step-d send layout, member block c)
@@ -527,6 +572,8 @@ class SpttEngine:
             dsend[r] = gd
             drecv[r] = self.buf[r]["grad_x"]
         for g in ([] if self.p2p_d else self._groups(p.group_of)):
+            if any(self.direct_x.get(r) for r in g):
+                continue  # one-rank tower: dX already is the gradient layout
             with self._t("exchange_d_bwd"):
                 fab.alltoallv(g, "d_bwd", dsend, {r: p.d_recv_splits(r) for r in g}, drecv,
                               {r: p.d_send_splits(r) for r in g})

@@ -234,26 +234,37 @@ class TowerModule:
                    rows_per_group=self.F, ld_group=O, ld_d=cD)
 
     # -- backward --------------------------------------------------------------
-    def backward(self, gy: torch.Tensor, fused_lr: Optional[float] = None) -> torch.Tensor:
+    def backward(self, gy: torch.Tensor, fused_lr: Optional[float] = None,
+                 dx_out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Returns dX (rows, F*N) in the compute dtype; fp32 weight grads are
         stored in ``self.grads`` (this rank's contribution only).
 
         ``fused_lr``: when no cross-rank gradient reduction is needed (a tower
         of one rank), the DCN weight matrices are updated in place by the dW
         GEMM epilogue (W -= lr * dW, dmt_gemm SCALE_ACC + ACC) and only the
-        bias grads are left in ``self.grads``."""
+        bias grads are left in ``self.grads``.  ``dx_out``: write dX there (a
+        persistent buffer the embedding backward reads directly)."""
         if self._saved is None:
             raise DomainError("backward() needs forward(save=True)")
+        self._dx_out = dx_out
         if self.cfg.kind == DLRM:
             return self._dlrm_bwd(gy)
         return self._dcn_bwd(gy, fused_lr)
+
+    def _new_dx(self, like: torch.Tensor) -> torch.Tensor:
+        out = getattr(self, "_dx_out", None)
+        if out is None:
+            return torch.empty_like(like)
+        if out.shape != like.shape or out.dtype != like.dtype:
+            raise ShapeError(f"dx_out {tuple(out.shape)} {out.dtype} does not match dX {tuple(like.shape)} {like.dtype}")
+        return out
 
     def _dlrm_bwd(self, gy):
         (x,) = self._saved
         c, p, D = self.cfg.per_feature_outputs, self.cfg.flat_outputs, self.cfg.out_dim
         rows, O, F, N = x.shape[0], self.width, self.F, self.N
         pD, cD = p * D, c * D
-        dx = torch.empty_like(x)
+        dx = self._new_dx(x)
         first = True
         f32 = torch.float32
         if pD:
@@ -331,7 +342,7 @@ class TowerModule:
                aux=gu[(L_ - 1) % 2], aux2=dx0, aux2_accum=False, colsum_part=part)
         weight_grad("w_proj", gy, xs[-1])
         self.grads["b_proj"] = K.column_sum(gy)
-        dx = torch.empty_like(g)
+        dx = self._new_dx(g)
         for layer in range(L_ - 1, -1, -1):
             cur = gu[layer % 2]
             bias_grad(f"b{layer}", cur)  # before the next GEMM overwrites the partials
@@ -378,7 +389,7 @@ class TowerModule:
                colsum_part=part)
         weight_grad("w_proj", gy, xs[-1])
         self.grads["b_proj"] = K.column_sum(gy)
-        dx = torch.empty_like(x0)
+        dx = self._new_dx(x0)
         for layer in range(L_ - 1, -1, -1):
             cur = gu[layer % 2]
             bias_grad(f"b{layer}", cur)  # before the next GEMM overwrites the partials
