@@ -147,7 +147,9 @@ def test_tower_module_backward_vs_oracle(kind, F, N, layers, dt, form, monkeypat
 @pytest.mark.parametrize("hosts,rph,kind,scheme,opt", [
     (2, 2, "dlrm", "table_wise", "sgd"), (2, 4, "dcn", "table_wise", "sgd"), (4, 2, "dcn", "table_wise", "sgd"),
     (1, 1, "dcn", "table_wise", "sgd"), (2, 2, "dcn", "column_wise", "sgd"), (2, 2, "dcn", "row_wise", "sgd"),
-    (2, 2, "dlrm", "table_wise", "adagrad"), (2, 4, "dcn", "column_wise", "adagrad")])
+    (2, 2, "dlrm", "table_wise", "adagrad"), (2, 4, "dcn", "column_wise", "adagrad"),
+    # one-rank towers (W = 1): lookup -> X and dX -> embedding backward in place
+    (2, 1, "dcn", "column_wise", "sgd"), (4, 1, "dlrm", "table_wise", "adagrad"), (2, 1, "dcn", "row_wise", "sgd")])
 def test_sptt_train_step_loopback_vs_oracle(hosts, rph, kind, scheme, opt):
     """Full step on G simulated ranks: outputs, then every table row after the
     optimizer (SGD or row-wise Adagrad), for table/column/row-wise shards."""
@@ -185,6 +187,8 @@ def test_sptt_train_step_loopback_vs_oracle(hosts, rph, kind, scheme, opt):
     grads = {r: torch.from_numpy(rng.normal(size=(B, O)).astype(np.float32)).to(dev()) for r in range(G)}
     outs = model.train_step(kjts, grads)
     torch.cuda.synchronize()
+    # the direct-X path is taken exactly for one-rank towers without row-wise shards
+    assert bool(model.engine.direct_x) == (rph == 1 and scheme != "row_wise")
 
     shards = [(s.table_id, s.rank, s.scheme, s.row_range, s.col_range) for s in placement.shards]
     flat, _, _, _ = oracle.baseline_forward(lens, vals, list(range(F)), pooling, before, shards,
