@@ -180,6 +180,7 @@ class SpttEngine:
         self._side = None
         self._prepared: dict = {}
         self.p2p_d = self.p2p_f = False
+        self.direct_peer_x = False
         if getattr(fabric, "p2p", False) and sptt:
             self._init_peer_links()
 
@@ -195,18 +196,28 @@ class SpttEngine:
         b = self.buf[r]
         self.p2p_d = p.W > 1
         self.p2p_f = p.T > 1
-        share = {"recv_d": b["recv_d"], "recv_f": b["recv_f"], "grad_x": b["grad_x"]}
+        share = {"recv_d": b["recv_d"], "recv_f": b["recv_f"], "grad_x": b["grad_x"], "X": b["X"]}
         if self.p2p_f:
             share["g_y"] = self._persist(r, "g_y", b["Y"])
         self.peer = self.fabric.share(share)
         if self.p2p_d:
+            # without row-wise shards (no summed pieces) the lookup stores each
+            # block straight into the member's TM input X (step e regroup
+            # fused too); otherwise into its step-d receive buffer
+            blocks = p.e_blocks(r)  # same feature layout for every member of the tower
+            self.direct_peer_x = not any(fb.rowwise for fb in blocks)
+            where = {pc.sid: fb.dst_col + pc.c0 for fb in blocks for pc in fb.pieces}
+            xw = p.x_width(r)
             segs = []
             for seg, (pp, k, off, w) in zip(self.seg_fwd[r].segments, p.lookup_out_offsets(r, True)):
                 c, j = pp % p.W, pp // p.W
                 m = p.tower_of(r) * p.W + c
-                dst = self.peer[m]["recv_d"]
-                segs.append(K.Segment(weights=seg.weights, out=dst, out_offset=p.d_recv_offset(m, r, k) + j * p.B * w,
-                                      out_ld=w, bag_begin=seg.bag_begin, nbags=seg.nbags, pooling=seg.pooling,
+                if self.direct_peer_x:
+                    dst, doff, dld = self.peer[m]["X"], j * p.B * xw + where[p.by_owner[r][k]], xw
+                else:
+                    dst, doff, dld = self.peer[m]["recv_d"], p.d_recv_offset(m, r, k) + j * p.B * w, w
+                segs.append(K.Segment(weights=seg.weights, out=dst, out_offset=doff,
+                                      out_ld=dld, bag_begin=seg.bag_begin, nbags=seg.nbags, pooling=seg.pooling,
                                       row_begin=seg.row_begin, row_filter=seg.row_filter, key_base=seg.key_base))
             self.seg_fwd_p2p = K.SegmentTable(segs, dev)
 
@@ -399,7 +410,7 @@ class SpttEngine:
                               {r: p.d_recv_splits(r) for r in g}, None)
         # step e: regroup + tower module
         for r in self.local:
-            if not self.direct_x.get(r):
+            if not (self.direct_x.get(r) or self.direct_peer_x):
                 self.asm_e[r].run()
             t = p.tower_of(r)
             if t in self.tm:
