@@ -311,6 +311,17 @@ int dmt_bce_with_logits(const void* z, const float* y, int64_t n, int32_t dtype,
 int dmt_sgd_dense(void* w, const float* g, int64_t n, float lr, int32_t dtype,
                   dmt_stream_t stream);
 
+/* Tower gradient all-reduce fused with SGD over NVLink peer memory (replaces
+ * the NCCL all-reduce of TM gradients over the tower comm, SURVEY §8e "bwd",
+ * + dmt_sgd_dense): w -= lr * (g[0] + g[1] + ... + g[nsrc-1]), summed in that
+ * order in fp32.  g is a HOST array of nsrc device pointers (this rank's own
+ * buffer and IPC-mapped peer buffers, 16-byte aligned), nsrc <=
+ * DMT_MAX_PEER_SRCS; every member passing the same order gets bit-identical
+ * replicas.  The caller orders it after a barrier on the peers' writes. */
+#define DMT_MAX_PEER_SRCS 8
+int dmt_peer_sum_sgd(void* w, const float* const* g, int32_t nsrc, int64_t n, float lr, int32_t dtype,
+                     dmt_stream_t stream);
+
 /* dst (dtype_out) = src (dtype_in), n elements */
 int dmt_convert(const void* src, int32_t dtype_in, void* dst, int32_t dtype_out, int64_t n,
                 dmt_stream_t stream);

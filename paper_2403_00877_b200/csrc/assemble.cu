@@ -237,6 +237,35 @@ __global__ void sgd_dense_kernel(T* __restrict__ w, const float* __restrict__ g,
     w[i] = from_d<T>(to_d<T>(w[i]) - (double)lr * (double)g[i]);
 }
 
+// Tower gradient all-reduce + SGD over NVLink peer memory: every member sums
+// the members' fp32 gradients in tower-rank order (identical on all members)
+// and applies w -= lr * sum to its own replica.  16-byte peer loads.
+struct PeerSrcs {
+  const float* g[DMT_MAX_PEER_SRCS];
+};
+
+template <typename T>
+__global__ void peer_sum_sgd_kernel(T* __restrict__ w, const __grid_constant__ PeerSrcs src, int nsrc, int64_t n,
+                                    float lr) {
+  const int64_t n4 = n >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 s = reinterpret_cast<const float4*>(src.g[0])[i];
+    for (int m = 1; m < nsrc; ++m) {
+      const float4 x = reinterpret_cast<const float4*>(src.g[m])[i];
+      s.x += x.x; s.y += x.y; s.z += x.z; s.w += x.w;
+    }
+    const float v[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) w[4 * i + e] = from_d<T>(to_d<T>(w[4 * i + e]) - (double)lr * (double)v[e]);
+  }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float s = src.g[0][i];
+    for (int m = 1; m < nsrc; ++m) s += src.g[m][i];
+    w[i] = from_d<T>(to_d<T>(w[i]) - (double)lr * (double)s);
+  }
+}
+
 template <typename A, typename B>
 __global__ void convert_kernel(const A* __restrict__ a, B* __restrict__ b, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -424,6 +453,28 @@ int dmt_sgd_dense(void* w, const float* g, int64_t n, float lr, int32_t dtype, d
     case DMT_F32: dmt::sgd_dense_kernel<float><<<grid, 256, 0, s>>>((float*)w, g, n, lr); break;
     case DMT_BF16: dmt::sgd_dense_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)w, g, n, lr); break;
     case DMT_F64: dmt::sgd_dense_kernel<double><<<grid, 256, 0, s>>>((double*)w, g, n, lr); break;
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_peer_sum_sgd(void* w, const float* const* g, int32_t nsrc, int64_t n, float lr, int32_t dtype,
+                     dmt_stream_t stream) {
+  if (n < 0 || nsrc < 1 || nsrc > DMT_MAX_PEER_SRCS || !g) return DMT_ERR_SHAPE;
+  if (n == 0) return DMT_OK;
+  dmt::PeerSrcs src{};
+  for (int m = 0; m < nsrc; ++m) {
+    if (!g[m] || (reinterpret_cast<uintptr_t>(g[m]) & 15)) return DMT_ERR_SHAPE;
+    src.g[m] = g[m];
+  }
+  // a small grid: runs beside the embedding-backward apply kernel
+  unsigned grid = (unsigned)std::min<int64_t>(dmt::ceil_div(dmt::ceil_div(n, 4), 256), DMT_NUM_SMS);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case DMT_F32: dmt::peer_sum_sgd_kernel<float><<<grid, 256, 0, s>>>((float*)w, src, nsrc, n, lr); break;
+    case DMT_BF16: dmt::peer_sum_sgd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)w, src, nsrc, n, lr); break;
+    case DMT_F64: dmt::peer_sum_sgd_kernel<double><<<grid, 256, 0, s>>>((double*)w, src, nsrc, n, lr); break;
     default: return DMT_ERR_UNSUPPORTED;
   }
   DMT_CHECK_LAUNCH();

@@ -452,6 +452,19 @@ def sgd_dense(w: torch.Tensor, g: torch.Tensor, lr: float) -> None:
             "dmt_sgd_dense")
 
 
+def peer_sum_sgd(w: torch.Tensor, grads: list, lr: float) -> None:
+    """w -= lr * sum(grads) (fp32, summed in list order); ``grads`` are this
+    rank's and peer-mapped (PeerBuffer) gradient buffers of w's size."""
+    import ctypes as C
+
+    for g in grads:
+        if g.dtype != torch.float32 or g.numel() != w.numel():
+            raise DomainError("peer gradients must be fp32 buffers of the weight's size")
+    arr = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
+    L.check(L.lib().dmt_peer_sum_sgd(w.data_ptr(), arr, len(grads), w.numel(), lr, _dt(w), L.stream_ptr()),
+            "dmt_peer_sum_sgd")
+
+
 def convert(x: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
     out = torch.empty(x.shape, dtype=dtype, device=x.device)
     L.check(L.lib().dmt_convert(x.data_ptr(), _dt(x), out.data_ptr(), _dt(out), x.numel(), L.stream_ptr()),

@@ -179,7 +179,7 @@ class SpttEngine:
         self.uniform_nnz = False
         self._side = None
         self._prepared: dict = {}
-        self.p2p_d = self.p2p_f = False
+        self.p2p_d = self.p2p_f = self.p2p_tm = False
         self.direct_peer_x = False
         if getattr(fabric, "p2p", False) and sptt:
             self._init_peer_links()
@@ -199,6 +199,14 @@ class SpttEngine:
         share = {"recv_d": b["recv_d"], "recv_f": b["recv_f"], "grad_x": b["grad_x"], "X": b["X"]}
         if self.p2p_f:
             share["g_y"] = self._persist(r, "g_y", b["Y"])
+        # TM gradients of a multi-rank tower: persistent fp32 buffers the tower
+        # members read over NVLink (all-reduce fused with the SGD step)
+        t = p.tower_of(r)
+        self.p2p_tm = p.W > 1 and t in self.tm
+        self.tm_gbuf = {}
+        if self.p2p_tm:
+            self.tm_gbuf = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in self.tm[t].w.items()}
+            share.update({"tmg_" + k: v for k, v in self.tm_gbuf.items()})
         self.peer = self.fabric.share(share)
         if self.p2p_d:
             # without row-wise shards (no summed pieces) the lookup stores each
@@ -549,7 +557,10 @@ class SpttEngine:
                                                 dx_out=self.buf[r]["gX"] if self.direct_x.get(r) else None)
                 acc = tower_grads.setdefault(t, {})
                 for k, v in self.tm[t].grads.items():
-                    acc[k] = v.clone() if k not in acc else acc[k].add_(v)
+                    if self.p2p_tm:  # one rank per process: into the peer-shared buffer
+                        acc[k] = self.tm_gbuf[k].view(v.shape).copy_(v)
+                    else:
+                        acc[k] = v.clone() if k not in acc else acc[k].add_(v)
             else:
                 dX[r] = grecv[r]
         # d^-1: scatter dX columns back into the step-d receive layout
@@ -592,6 +603,18 @@ class SpttEngine:
         def tm_reduce_and_step():
             for t, grads in tower_grads.items():
                 group = p.layout.tower_ranks(t, p.topo)
+                if self.p2p_tm:
+                    # NVLink: after the barrier every member sums the members'
+                    # gradient buffers in tower-rank order into its own replica
+                    # (identical on all members).  A member overwrites its
+                    # buffer only after the next step's step-d barrier, which
+                    # every reader passes after this side stream is joined.
+                    fab.barrier_(group)
+                    for k, g in grads.items():
+                        K.peer_sum_sgd(self.tm[t].w[k], [self.peer[m]["tmg_" + k] for m in group],
+                                       tm_lr if tm_lr is not None else lr)
+                    self.tm[t].grads = grads
+                    continue
                 fab.all_reduce_(group, grads)
                 self.tm[t].grads = grads
                 self.tm[t].sgd_step(tm_lr if tm_lr is not None else lr)

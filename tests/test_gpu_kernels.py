@@ -252,3 +252,27 @@ def test_column_sum_vs_fp64(rows, cols, dt):
     torch.cuda.synchronize()
     assert torch.equal(got, again)
     assert (got.double() - want).abs().max().item() <= 1e-5 * (x.double().abs().sum(0).max().item() + 1)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("nsrc,n", [(1, 5), (2, 1664 * 1664 + 3), (3, 4096), (4, 832)])
+def test_peer_sum_sgd_matches_rank_order_sum(dt, nsrc, n):
+    """dmt_peer_sum_sgd (tower all-reduce + SGD over peer memory) == the
+    loopback engine's rank-order fp32 sum followed by dmt_sgd_dense, bit for
+    bit (local buffers stand in for the IPC-mapped peers)."""
+    from paper_2403_00877_b200 import kernels as K
+    from paper_2403_00877_b200.errors import DomainError
+
+    gen = torch.Generator(device="cpu").manual_seed(n + nsrc)
+    w0 = torch.randn(n, generator=gen).to(dev(), dt)
+    gs = [torch.randn(n, generator=gen).to(dev()) for _ in range(nsrc)]
+    want = w0.clone()
+    acc = gs[0].clone()
+    for g in gs[1:]:
+        acc.add_(g)
+    K.sgd_dense(want, acc, 0.05)
+    got = w0.clone()
+    K.peer_sum_sgd(got, gs, 0.05)
+    assert torch.equal(got, want)
+    with pytest.raises(DomainError):
+        K.peer_sum_sgd(got, [g.to(torch.bfloat16) for g in gs], 0.05)
