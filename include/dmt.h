@@ -282,7 +282,7 @@ int dmt_gemm(const dmt_gemm_args* args, dmt_stream_t stream);
 int dmt_gemm_ex(const dmt_gemm_args* args, const void* a_lo, const void* b_lo,
                 dmt_stream_t stream);
 
-/* hi = x with the 13 low mantissa bits cleared (exact tf32), lo = x - hi. */
+/* hi = tf32(x) (round to nearest), lo = tf32(x - hi): the 3xTF32 operand split. */
 int dmt_split_tf32(const float* x, float* hi, float* lo, int64_t n, dmt_stream_t stream);
 
 /* out[j, i] = in[i, j]  (rows x cols, row strides ld_in / ld_out) */

@@ -41,10 +41,15 @@ static int dispatch_major(const dmt_gemm_args* a, const void* alo, const void* b
 __global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo,
                                   int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float v = x[i];
-    float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-    hi[i] = h;
-    lo[i] = v - h;
+    // round-to-nearest split: hi = tf32(v), lo = tf32(v - hi) (exact residual,
+    // then rounded, so the MMA's tf32 read of lo drops nothing)
+    const float v = x[i];
+    uint32_t h, l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+    const float r = v - __uint_as_float(h);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+    hi[i] = __uint_as_float(h);
+    lo[i] = __uint_as_float(l);
   }
 }
 

@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -144,6 +145,24 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 registers per thread -> 32 lanes x 32 columns of 32-bit TMEM.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])),
+      "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])), "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])),
+      "r"(__float_as_uint(v[20])), "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])), "r"(__float_as_uint(v[27])),
+      "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])), "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // SM100 shared-memory matrix descriptor, K-major, SWIZZLE_128B:
 //   [0,14) start>>4  [16,30) LBO>>4 (unused for swizzled K-major)
 //   [32,46) SBO>>4 = 1024 B between 8-row core groups   [46,48) version = 1
@@ -237,6 +256,7 @@ struct Params {
   const void* pg[DMT_GEMM_MAX_PAIRS];
   const void* pu[DMT_GEMM_MAX_PAIRS];
   float* colsum;  // DCN_BWD: per (128-row tile, 32-row quarter) column sums of the stored gu
+  int kchunk;     // tf32: K blocks accumulated per TMEM chunk (see gemm_kernel)
 };
 
 // Output row address.  The grouped layout (per-feature DLRM projection rows
@@ -539,7 +559,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   constexpr int B_BYTES = BN * kAtomBytes;
   constexpr int NSETS = (NOPS == 3) ? 2 : 1;  // hi (+ lo) operand copies
   constexpr int STAGE_BYTES = NSETS * (A_BYTES + B_BYTES);
-  constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  // tf32 (fp32 parity path): two accumulators + two chunk-scratch buffers
+  constexpr int ACC_BUFS = (KIND == 1) ? 4 : 2;
+  constexpr uint32_t TMEM_COLS = (ACC_BUFS * BN <= 32) ? 32 : (ACC_BUFS * BN <= 64 ? 64 :
+                                 (ACC_BUFS * BN <= 128 ? 128 : (ACC_BUFS * BN <= 256 ? 256 : 512)));
+  static_assert(ACC_BUFS * BN <= 512, "TMEM columns");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -547,7 +571,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;   // tf32 chunk scratch buffers: MMA -> epilogue
+  uint64_t* sempty = sfull + 2;   //                             epilogue -> MMA
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + 2);
   float* stile_all = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -571,6 +597,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], kEpiWarps);  // one arrive per epilogue warp
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -629,13 +657,31 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      int s_it = 0;  // tf32 chunk-scratch uses
       for (int64_t u = u_first; u < num_units; u += u_step, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
+        // tf32: the tensor core's accumulation truncates, so a long K chain
+        // drifts (measured ~3e-5 max-norm relative at K = 3328, 10x fp32's).
+        // Every p.kchunk K blocks start a fresh accumulation in a scratch TMEM
+        // buffer; the epilogue warps fold it into the tile's accumulator with
+        // round-to-nearest fp32 adds in chunk order (deterministic).
+        uint32_t tmem_t = tmem_d;
+        bool first = true;
         for (int kb = 0; kb < num_kb; ++kb) {
+          if constexpr (KIND == 1) {
+            if (kb > 0 && kb % p.kchunk == 0) {
+              if (tmem_t != tmem_d) umma_commit(&sfull[(s_it - 1) & 1]);  // previous chunk complete
+              mbar_wait(&sempty[s_it & 1], ((s_it >> 1) & 1) ^ 1);
+              tc_fence_after();
+              tmem_t = tmem_base + (2 + (s_it & 1)) * BN;
+              ++s_it;
+              first = true;
+            }
+          }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -645,15 +691,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
 #pragma unroll
           for (int kk = 0; kk < kAtomBytes / kUmmaKBytes; ++kk) {
             const uint64_t ada = OA::kstep(kk), adb = OB::kstep(kk);
-            const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
-            umma<KIND>(tmem_d, da + ada, db + adb, idesc, accum);
+            const uint32_t accum = (first && kk == 0) ? 0u : 1u;
+            umma<KIND>(tmem_t, da + ada, db + adb, idesc, accum);
             if constexpr (NSETS == 2) {
               uint8_t* sa2 = sb + B_BYTES;
               uint8_t* sb2 = sa2 + A_BYTES;
               const uint64_t da2 = OA::desc(smem_u32(sa2));
               const uint64_t db2 = OB::desc(smem_u32(sb2));
-              umma<KIND>(tmem_d, da + ada, db2 + adb, idesc, 1u);  // hi * lo
-              umma<KIND>(tmem_d, da2 + ada, db + adb, idesc, 1u);  // lo * hi
+              umma<KIND>(tmem_t, da + ada, db2 + adb, idesc, 1u);  // hi * lo
+              umma<KIND>(tmem_t, da2 + ada, db + adb, idesc, 1u);  // lo * hi
             }
           }
           // smem slot reusable once these MMAs retire (in every cluster CTA:
@@ -661,6 +707,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           if constexpr (CL > 1) umma_commit_mc(&empty[stage], 0x3);
           else umma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          first = false;
+        }
+        if constexpr (KIND == 1) {
+          if (tmem_t != tmem_d) umma_commit(&sfull[(s_it - 1) & 1]);
         }
         umma_commit(&tfull[acc]);  // accumulator complete
       }
@@ -671,12 +721,34 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     const int half = (warp - 2) / 4;              // which half of the tile's columns
     constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
     int it = 0;
+    int e_it = 0;  // tf32 chunk-scratch uses (mirrors the MMA warp's s_it)
     for (int64_t u = u_first; u < num_units; u += u_step, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int64_t m0 = unit_m0(u);
       const int64_t n0 = unit_n0(u);
       float* stile = stile_all + (warp - 2) * kStileFloats;
+      if constexpr (KIND == 1) {
+        // fold chunks 1.. of this tile into its accumulator (chunk order)
+        const int nch = (num_kb + p.kchunk - 1) / p.kchunk;
+        const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+        for (int c = 1; c < nch; ++c, ++e_it) {
+          mbar_wait(&sfull[e_it & 1], (e_it >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int col = half * kColsPerWarp; col < (half + 1) * kColsPerWarp; col += 32) {
+            float v[32], w[32];
+            tmem_ld32(lane_base + (uint32_t)((2 + (e_it & 1)) * BN + col), v);
+            tmem_ld32(lane_base + (uint32_t)(acc * BN + col), w);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) w[i] += v[i];
+            tmem_st32(lane_base + (uint32_t)(acc * BN + col), w);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sempty[e_it & 1]);
+        }
+      }
       if (p.coalesced && n0 + (int64_t)(half + 1) * kColsPerWarp <= p.n) {
         // Pipelined full-width path: the epilogue operands (x0 / u / C / dx0)
         // do not depend on the accumulator, so the loads of slab-pair k+1 are
@@ -984,6 +1056,17 @@ static bool make_plain_map(CUtensorMap* map, const void* ptr, int64_t rows, int6
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// tf32 accumulation chunk in 32-element K blocks (DMT_TF32_KCHUNK overrides;
+// measured: tools/fp32_accuracy.py)
+static int tf32_kchunk() {
+  static int kc = [] {
+    const char* e = getenv("DMT_TF32_KCHUNK");
+    int v = e ? atoi(e) : 4;
+    return v > 0 ? v : 1 << 30;
+  }();
+  return kc;
+}
+
 template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN, bool FEAT,
           int CL = 1>
 static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cudaStream_t s) {
@@ -1021,6 +1104,7 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   p.aux2_accum = (a->flags & DMT_GEMM_AUX2_ACCUM) != 0;
   p.scale_acc = (a->flags & DMT_GEMM_SCALE_ACC) != 0;
   p.alpha = a->alpha;
+  p.kchunk = tf32_kchunk();
   p.beta = a->beta; p.out_dtype = a->out_dtype; p.in_dtype = a->in_dtype; p.epilogue = a->epilogue;
   size_t eo = dtype_size(a->out_dtype);
   p.vec_store = ((uintptr_t)a->d % 16 == 0) && ((a->ld_d * eo) % 16 == 0) && ((a->ld_group * eo) % 16 == 0);

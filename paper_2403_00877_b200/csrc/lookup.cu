@@ -832,9 +832,349 @@ int launch_async_update(const uint32_t* keys, const int32_t* vals, int64_t nnz, 
   return DMT_OK;
 }
 
+// ---- bucketed backward (the default fast path) -----------------------------
+// Prepare (needs only the indices; runs on a side stream under the tower
+// module): every valid occurrence's sort key (shard key base + row) is
+// counted into its bucket of 2^bshift consecutive keys, the counts are
+// scanned, and each occurrence is scattered into its bucket as one 64-bit item
+// (key << 32 | 16-byte offset of its gradient row).  Apply (needs the
+// gradients): each CTA takes whole buckets, sorts a bucket's items in shared
+// memory by (key, gradient row) -- a canonical order, so the update does not
+// depend on the scatter's arrival order (deterministic, no float atomics) --
+// compacts the run heads (one per unique row), and every thread group reduces
+// one run in that order and applies SGD / row-wise Adagrad to the row once.
+// Replaces the 25-bit CUB radix sort + the key -> shard -> row dependent chain
+// of the earlier apply: rows of a bucket are resolved from shared memory.
+constexpr int kBktThreads = 256;
+constexpr int kBktCap = 2048;  // items of one bucket sorted in shared memory at once
+
+inline int bucket_shift(int64_t nnz, int64_t key_space) {
+  // widest bucket whose mean population (uniform keys) stays <= 1024 items
+  int s = 4;
+  const double dens = (double)std::max<int64_t>(nnz, 1) / (double)std::max<int64_t>(key_space, 1);
+  while (s < 20 && dens * (double)(1ll << (s + 1)) <= 1024.0) ++s;
+  return s;
+}
+
+inline int64_t bucket_count(int64_t key_space, int bshift) { return (key_space >> bshift) + 1; }
+
+__global__ void bwd_bucket_keys_kernel(const dmt_lookup_segment* __restrict__ segs,
+                                       const int64_t* __restrict__ offsets, const int32_t* __restrict__ indices,
+                                       uint32_t invalid, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                                       const char* __restrict__ gbase, int es, int bshift,
+                                       uint32_t* __restrict__ counts) {
+  const dmt_lookup_segment& sg = segs[blockIdx.y];
+  const int sub = threadIdx.x & 7;
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  if (b >= sg.nbags) return;
+  const int64_t gb = sg.bag_begin + b;
+  const int64_t beg = offsets[gb], end = offsets[gb + 1];
+  const int32_t goff = (int32_t)((reinterpret_cast<const char*>(sg.out) + (size_t)(b * sg.out_ld) * es - gbase) >> 4);
+  for (int64_t k = beg + sub; k < end; k += 8) {
+    const int64_t r = (int64_t)__ldg(indices + k) - sg.row_begin;
+    const bool in = r >= 0 && r < sg.rows;
+    const uint32_t key = in ? (uint32_t)(sg.key_base + r) : invalid;
+    keys[k] = key;
+    vals[k] = goff;
+    if (in) atomicAdd(counts + (key >> bshift), 1u);
+  }
+}
+
+// exclusive scan of counts[0, n) into offs[0, n]; cursor = offs (one CTA)
+__global__ void __launch_bounds__(1024) bucket_scan_kernel(const uint32_t* __restrict__ counts, int64_t n,
+                                                           uint32_t* __restrict__ offs, uint32_t* __restrict__ cursor) {
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t base = 0; base < n; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const uint32_t v = i < n ? counts[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t t = warp_tot[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_tot[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint32_t excl = carry + (wid ? warp_tot[wid - 1] : 0u) + x - v;
+    if (i < n) {
+      offs[i] = excl;
+      cursor[i] = excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) offs[n] = carry;
+}
+
+__global__ void bwd_bucket_scatter_kernel(const uint32_t* __restrict__ keys, const int32_t* __restrict__ vals,
+                                          int64_t nnz, uint32_t invalid, int bshift, uint32_t* __restrict__ cursor,
+                                          uint64_t* __restrict__ items) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t key = __ldg(keys + k);
+    if (key == invalid) continue;
+    const uint32_t pos = atomicAdd(cursor + (key >> bshift), 1u);
+    items[pos] = ((uint64_t)key << 32) | (uint32_t)__ldg(vals + k);
+  }
+}
+
+// in-place ascending bitonic sort of s[0, P), P a power of two (block-wide)
+__device__ __forceinline__ void bitonic_smem(uint64_t* s, int P) {
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t a = s[i], b = s[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            s[i] = b;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// the same over global memory (oversized buckets: skewed / hot keys), with
+// the strides below kBktCap done in shared memory per chunk
+__device__ void bitonic_global(uint64_t* g, int64_t P, uint64_t* s) {
+  const int C = kBktCap;
+  auto local_stages = [&](int64_t k, int jmax) {
+    // strides jmax..1 of merge level k, chunk by chunk through shared memory
+    for (int64_t c0 = 0; c0 < P; c0 += C) {
+      for (int i = threadIdx.x; i < C; i += blockDim.x) s[i] = g[c0 + i];
+      __syncthreads();
+      for (int j = jmax; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < C; i += blockDim.x) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const uint64_t a = s[i], b = s[ixj];
+            if ((a > b) == (((c0 + i) & k) == 0)) {
+              s[i] = b;
+              s[ixj] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      for (int i = threadIdx.x; i < C; i += blockDim.x) g[c0 + i] = s[i];
+      __syncthreads();
+    }
+  };
+  for (int64_t k = 2; k <= P; k <<= 1) {
+    int64_t j = k >> 1;
+    for (; j >= C; j >>= 1) {
+      for (int64_t i = threadIdx.x; i < P; i += blockDim.x) {
+        const int64_t ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t a = g[i], b = g[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            g[i] = b;
+            g[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    local_stages(k, (int)j);
+  }
+}
+
+template <typename T, int VEC, int NV>
+__global__ void __launch_bounds__(kBktThreads, 4)
+bwd_bucket_apply_kernel(const uint64_t* __restrict__ items, const uint32_t* __restrict__ boff, int64_t nbuckets,
+                        uint64_t* __restrict__ scratch, const char* __restrict__ gbase,
+                        const __grid_constant__ ShardTab tab, int log2g, int opt, float lr, float eps) {
+  using A = typename Acc<T>::type;
+  __shared__ uint64_t s_items[kBktCap];
+  __shared__ uint16_t s_run[kBktCap + 1];
+  __shared__ uint32_t s_wsum[kBktThreads / 32];
+  __shared__ int s_nruns;
+  __shared__ uint32_t s_kb[kMaxShards];
+  __shared__ uint16_t s_ld[kMaxShards], s_w[kMaxShards];
+  __shared__ const char* s_wp[kMaxShards];
+  __shared__ float* s_st[kMaxShards];
+  for (int i = threadIdx.x; i < tab.n; i += blockDim.x) {
+    s_kb[i] = tab.key_base[i];
+    s_ld[i] = tab.ld[i];
+    s_w[i] = tab.width[i];
+    s_wp[i] = tab.weights[i];
+    s_st[i] = tab.state[i];
+  }
+  __syncthreads();
+  const int nsh = tab.n;
+  const int G = 1 << log2g;
+  const int t = threadIdx.x & (G - 1);
+  const int gid = threadIdx.x >> log2g;
+  const int ngroups = kBktThreads >> log2g;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int E = kBktCap / kBktThreads;  // window items per thread in the head scan
+
+  for (int64_t bk = blockIdx.x; bk < nbuckets; bk += gridDim.x) {
+    const int64_t beg = boff[bk];
+    const int64_t n = (int64_t)boff[bk + 1] - beg;
+    if (n == 0) continue;
+    const uint64_t* src;  // the bucket's items, sorted
+    if (n <= kBktCap) {
+      int P = 2;
+      while (P < n) P <<= 1;
+      for (int i = threadIdx.x; i < P; i += blockDim.x) s_items[i] = i < n ? items[beg + i] : ~0ull;
+      __syncthreads();
+      bitonic_smem(s_items, P);
+      src = nullptr;
+    } else {
+      int64_t P = kBktCap;
+      while (P < n) P <<= 1;
+      uint64_t* g = scratch + 2 * beg;  // P <= 2n: disjoint per bucket
+      for (int64_t i = threadIdx.x; i < P; i += blockDim.x) g[i] = i < n ? items[beg + i] : ~0ull;
+      __syncthreads();
+      bitonic_global(g, P, s_items);
+      src = g;
+    }
+    for (int64_t w0 = 0; w0 < n; w0 += kBktCap) {
+      const int wn = (int)(n - w0 < kBktCap ? n - w0 : (int64_t)kBktCap);
+      if (src) {
+        for (int i = threadIdx.x; i < wn; i += blockDim.x) s_items[i] = src[w0 + i];
+        __syncthreads();
+      }
+      const uint32_t prev_key = w0 > 0 ? (uint32_t)(src[w0 - 1] >> 32) : 0xFFFFFFFFu;
+      // run heads of the window -> s_run[0, nruns) (block scan of head flags)
+      uint32_t cnt = 0;
+      bool hd[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = threadIdx.x * E + e;
+        hd[e] = false;
+        if (i < wn) {
+          const uint32_t k = (uint32_t)(s_items[i] >> 32);
+          const uint32_t kp = i ? (uint32_t)(s_items[i - 1] >> 32) : prev_key;
+          hd[e] = k != kp;
+        }
+        cnt += hd[e];
+      }
+      uint32_t x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_wsum[wid] = x;
+      __syncthreads();
+      uint32_t before = x - cnt;
+      for (int w = 0; w < wid; ++w) before += s_wsum[w];
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (hd[e]) s_run[before++] = (uint16_t)(threadIdx.x * E + e);
+      if (threadIdx.x == kBktThreads - 1) s_nruns = (int)before;
+      __syncthreads();
+      const int nruns = s_nruns;
+      // one run (= one unique row) per thread group; warp-uniform trip count
+      // (the Adagrad reduction shuffles across the whole warp)
+      const int gpw = 32 >> log2g;
+      for (int rb = (gid / gpw) * gpw; rb < nruns; rb += ngroups) {
+        const int r = rb + gid % gpw;
+        if (r >= nruns) continue;  // whole-group uniform; Adagrad below masks by active groups
+        const int i0 = s_run[r];
+        const uint32_t key = (uint32_t)(s_items[i0] >> 32);
+        int lo = 0, hi = nsh - 1;  // last shard with key_base <= key
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_kb[mid] <= key) lo = mid; else hi = mid - 1;
+        }
+        const int width = s_w[lo];
+        const int64_t row = (int64_t)(key - s_kb[lo]);
+        T* W = const_cast<T*>(reinterpret_cast<const T*>(s_wp[lo])) + row * s_ld[lo];
+        Frag<T, VEC> w[NV], g0[NV];
+        const T* gp0 = reinterpret_cast<const T*>(gbase + ((int64_t)(uint32_t)s_items[i0] << 4));
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int c = (v * G + t) * VEC;
+          if (c < width) {
+            w[v].load(W + c);
+            g0[v].load(gp0 + c);
+          } else {
+            w[v].zero();
+            g0[v].zero();
+          }
+        }
+        A acc[NV][VEC];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[v][e] = A(0);
+          g0[v].add_to(acc[v]);
+        }
+        // the rest of the run, in sorted order (may run past the window)
+        for (int64_t j = w0 + i0 + 1; j < n; ++j) {
+          const uint64_t it = (j - w0 < wn) ? s_items[j - w0] : src[j];
+          if ((uint32_t)(it >> 32) != key) break;
+          const T* gp = reinterpret_cast<const T*>(gbase + ((int64_t)(uint32_t)it << 4));
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const int c = (v * G + t) * VEC;
+            if (c < width) {
+              A xx[VEC];
+              Loader<T, VEC>::load(gp + c, xx);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) acc[v][e] += xx[e];
+            }
+          }
+        }
+        A step = (A)lr;
+        if (opt == DMT_OPT_ROWWISE_ADAGRAD) {
+          float sq = 0.f;
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) sq += (float)(acc[v][e] * acc[v][e]);
+          const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+          for (int o = G >> 1; o > 0; o >>= 1) sq += __shfl_xor_sync(gmask, sq, o, G);
+          float* st = s_st[lo] + row;
+          const float s_new = *st + sq / (float)width;
+          step = (A)(lr / (sqrtf(s_new) + eps));
+          __syncwarp(__activemask());
+          if (t == 0) *st = s_new;
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int c = (v * G + t) * VEC;
+          if (c < width) {
+            A nw[VEC];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) nw[e] = A(0);
+            w[v].add_to(nw);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) nw[e] = nw[e] - step * acc[v][e];
+            Loader<T, VEC>::store(W + c, nw);
+          }
+        }
+      }
+      __syncthreads();  // s_items / s_run reused by the next window / bucket
+    }
+  }
+}
+
 struct BwdLayout {
   size_t keys_in, keys_out, vals_in, vals_out, recs, cub_temp, total;
   size_t cub_bytes;
+  size_t bcounts, boffs, bcursor, items, scratch;  // bucketed path
+  int bshift;
+  int64_t nbuckets;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -861,6 +1201,14 @@ inline BwdLayout bwd_layout(int64_t nnz, int64_t key_space, int64_t nbags) {
   L.vals_out = off; off = align256(off + n * 4);
   L.recs = off; off = align256(off + nb * sizeof(BagRec));
   L.cub_temp = off; off = align256(off + L.cub_bytes);
+  L.bshift = bucket_shift((int64_t)n, key_space);
+  L.nbuckets = bucket_count(key_space, L.bshift);
+  const size_t nbk = (size_t)L.nbuckets;
+  L.bcounts = off; off = align256(off + nbk * 4);
+  L.boffs = off; off = align256(off + (nbk + 1) * 4);
+  L.bcursor = off; off = align256(off + nbk * 4);
+  L.items = off; off = align256(off + n * 8);
+  L.scratch = off; off = align256(off + 2 * n * 8 + (size_t)kBktCap * 8);
   L.total = off;
   return L;
 }
@@ -885,6 +1233,14 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     if (hs[i].ld > 65535 || hs[i].width > 65535) return DMT_ERR_UNSUPPORTED;
   }
   if (max_b == 0) return DMT_OK;
+  // apply variants (DMT_BWD_VARIANT, read once so prepare and apply agree):
+  // 0 (default) bucketed sort + apply; 2 the earlier register kernel over a
+  // CUB radix sort (one occurrence per group, 4 CTAs / SM); 1 its
+  // two-occurrence form; 4 the bulk-copy staged kernel -- all parity-tested
+  static const int bwd_variant = [] {
+    const char* e = getenv("DMT_BWD_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
   // fast path: no mean pooling, 16-byte aligned gradient rows inside one
   // buffer (offset < 32 GB), <= kMaxShards distinct shards, vector widths
   constexpr int VEC0 = Vec16<T>::N;
@@ -937,7 +1293,24 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
   BagRec* recs = (BagRec*)(w + L.recs);
   const uint32_t invalid = (uint32_t)key_space;
 
-  if (phase & 1) {
+  const bool bucketed = fast && bwd_variant == 0;
+  uint32_t* bcounts = (uint32_t*)(w + L.bcounts);
+  uint32_t* boffs = (uint32_t*)(w + L.boffs);
+  uint32_t* bcursor = (uint32_t*)(w + L.bcursor);
+  uint64_t* items = (uint64_t*)(w + L.items);
+  uint64_t* scratch = (uint64_t*)(w + L.scratch);
+  if ((phase & 1) && bucketed) {
+    if (cudaMemsetAsync(bcounts, 0, (size_t)L.nbuckets * 4, s) != cudaSuccess) return DMT_ERR_CUDA;
+    dim3 kg((unsigned)ceil_div((int64_t)max_b * 8, 256), n);
+    bwd_bucket_keys_kernel<<<kg, 256, 0, s>>>(segs, offsets, indices, invalid, keys_in, vals_in, gbase,
+                                              (int)sizeof(T), L.bshift, bcounts);
+    DMT_CHECK_LAUNCH();
+    bucket_scan_kernel<<<1, 1024, 0, s>>>(bcounts, L.nbuckets, boffs, bcursor);
+    DMT_CHECK_LAUNCH();
+    const unsigned sg = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nnz, 256), DMT_NUM_SMS * 8));
+    bwd_bucket_scatter_kernel<<<sg, 256, 0, s>>>(keys_in, vals_in, nnz, invalid, L.bshift, bcursor, items);
+    DMT_CHECK_LAUNCH();
+  } else if (phase & 1) {
     dim3 kg((unsigned)ceil_div((int64_t)max_b * 8, 256), n);
     if (fast)
       bwd_keys_fast_kernel<<<kg, 256, 0, s>>>(segs, offsets, indices, invalid, keys_in, vals_in, gbase,
@@ -952,6 +1325,26 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
   }
   if (!(phase & 2)) return DMT_OK;
   constexpr int VEC = Vec16<T>::N;
+  if (bucketed) {
+    const int nvec = (max_w + VEC0 - 1) / VEC0;
+    int G = 1, log2g = 0;
+    while (G * 2 < nvec && G < 32) { G <<= 1; ++log2g; }
+    const int nv = (nvec + G - 1) / G;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(L.nbuckets, (int64_t)DMT_NUM_SMS * 4));
+    if (nv == 1)
+      bwd_bucket_apply_kernel<T, VEC0, 1><<<grid, kBktThreads, 0, s>>>(items, boffs, L.nbuckets, scratch, gbase,
+                                                                       tab, log2g, opt, lr, eps);
+    else if (nv == 2)
+      bwd_bucket_apply_kernel<T, VEC0, 2><<<grid, kBktThreads, 0, s>>>(items, boffs, L.nbuckets, scratch, gbase,
+                                                                       tab, log2g, opt, lr, eps);
+    else if (nv <= 4)
+      bwd_bucket_apply_kernel<T, VEC0, 4><<<grid, kBktThreads, 0, s>>>(items, boffs, L.nbuckets, scratch, gbase,
+                                                                       tab, log2g, opt, lr, eps);
+    else
+      return DMT_ERR_UNSUPPORTED;
+    DMT_CHECK_LAUNCH();
+    return DMT_OK;
+  }
   bool vec_ok = true;
   for (int i = 0; i < n; ++i) {
     const dmt_lookup_segment& g = hs[i];
@@ -968,10 +1361,6 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
   // tuning knob for the 16-bit apply: 0 (default) register kernel, one
   // occurrence per thread group at 4 CTAs / SM; 1 the earlier two-occurrence
   // form; 4 the bulk-copy staged kernel (all three parity-tested)
-  static const int bwd_variant = [] {
-    const char* e = getenv("DMT_BWD_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
   const bool async16 = sizeof(T) == 2 && bwd_variant == 4;
   if (fast && (sizeof(T) >= 4 || async16) && nvec_all * VEC == max_w &&
       (nvec_all == 8 || nvec_all == 16 || nvec_all == 32)) {

@@ -202,10 +202,15 @@ class SpttEngine:
         # TM gradients of a multi-rank tower: persistent fp32 buffers the tower
         # members read over NVLink (all-reduce fused with the SGD step)
         t = p.tower_of(r)
-        self.p2p_tm = p.W > 1 and t in self.tm
+        # (dmt_peer_sum_sgd sums at most DMT_MAX_PEER_SRCS members; wider
+        # towers keep the NCCL all-reduce + SGD)
+        self.p2p_tm = 1 < p.W <= L.MAX_PEER_SRCS and t in self.tm
         self.tm_gbuf = {}
         if self.p2p_tm:
-            self.tm_gbuf = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in self.tm[t].w.items()}
+            # zero-size weights (e.g. DLRM w_flat with flat_outputs = 0) have no
+            # gradient to exchange: a null pointer cannot be IPC-exported
+            self.tm_gbuf = {k: torch.empty(v.shape, dtype=torch.float32, device=dev)
+                            for k, v in self.tm[t].w.items() if v.numel()}
             share.update({"tmg_" + k: v for k, v in self.tm_gbuf.items()})
         self.peer = self.fabric.share(share)
         if self.p2p_d:
@@ -558,7 +563,7 @@ class SpttEngine:
                 acc = tower_grads.setdefault(t, {})
                 for k, v in self.tm[t].grads.items():
                     if self.p2p_tm:  # one rank per process: into the peer-shared buffer
-                        acc[k] = self.tm_gbuf[k].view(v.shape).copy_(v)
+                        acc[k] = self.tm_gbuf[k].view(v.shape).copy_(v) if v.numel() else v
                     else:
                         acc[k] = v.clone() if k not in acc else acc[k].add_(v)
             else:
@@ -611,9 +616,14 @@ class SpttEngine:
                     # every reader passes after this side stream is joined.
                     fab.barrier_(group)
                     for k, g in grads.items():
-                        K.peer_sum_sgd(self.tm[t].w[k], [self.peer[m]["tmg_" + k] for m in group],
-                                       tm_lr if tm_lr is not None else lr)
-                    self.tm[t].grads = grads
+                        if g.numel():
+                            K.peer_sum_sgd(self.tm[t].w[k], [self.peer[m]["tmg_" + k] for m in group],
+                                           tm_lr if tm_lr is not None else lr)
+                    # the tower-summed gradient is never materialised on this
+                    # path (each member folds the peers' buffers straight into
+                    # its weights): leave no rank-local partial behind that a
+                    # caller could mistake for the summed gradient
+                    self.tm[t].grads = {}
                     continue
                 fab.all_reduce_(group, grads)
                 self.tm[t].grads = grads

@@ -32,7 +32,10 @@ class SPTT:
                  feature_towers: dict, pooling: dict, local_batch: int, fabric: Fabric,
                  tm: Optional[object] = None, dtype: torch.dtype = torch.float32, device=None,
                  mode: str = "sptt", lr: float = 0.01, optimizer: str = "sgd", eps: float = 1e-8,
-                 trace=None, top: Optional[TMConfig] = None):
+                 trace=None, top: Optional[TMConfig] = None, dense_lr: Optional[float] = None):
+        """``lr`` drives the embedding (sparse) update; ``dense_lr`` (default:
+        ``lr``) the tower modules, the flat baseline's global TM and the top
+        head -- recommendation models train the two at very different rates."""
         self.topo, self.layout, self.placement = topo, layout, placement
         self.device = device or torch.device("cuda")
         feats = sorted(pooling)
@@ -79,6 +82,7 @@ class SPTT:
                                    device=self.device)
             self._labels_loss = {}
         self.lr, self.eps = lr, eps
+        self.dense_lr = lr if dense_lr is None else dense_lr
         self.opt = L.OPT_ROWWISE_ADAGRAD if optimizer == "adagrad" else L.OPT_SGD
         if self.opt == L.OPT_ROWWISE_ADAGRAD:
             self.engine.enable_adagrad()
@@ -103,7 +107,7 @@ class SPTT:
 
     def backward(self, grads: dict, dense_hook=None) -> None:
         if self.global_tm is None:
-            self.engine.backward(grads, self.lr, self.opt, self.eps, dense_hook=dense_hook)
+            self.engine.backward(grads, self.lr, self.opt, self.eps, tm_lr=self.dense_lr, dense_hook=dense_hook)
             return
         dx, acc = {}, {}
         for r, g in grads.items():
@@ -116,11 +120,11 @@ class SPTT:
         def dense_step():  # world all-reduce of the global TM grads + SGD
             self.fabric.all_reduce_(list(range(self.plan.G)), acc)
             self.global_tm.grads = acc
-            self.global_tm.sgd_step(self.lr)
+            self.global_tm.sgd_step(self.dense_lr)
             if dense_hook is not None:
                 dense_hook()
 
-        self.engine.backward(dx, self.lr, self.opt, self.eps, dense_hook=dense_step)
+        self.engine.backward(dx, self.lr, self.opt, self.eps, tm_lr=self.dense_lr, dense_hook=dense_step)
 
     def train_step(self, kjts: dict, grads: dict) -> dict:
         outs = self.forward(kjts, save=True)
@@ -155,7 +159,7 @@ class SPTT:
         def top_step():  # world all-reduce of the head's grads + SGD
             self.fabric.all_reduce_(list(range(self.plan.G)), acc)
             self.top.grads = acc
-            self.top.sgd_step(self.lr)
+            self.top.sgd_step(self.dense_lr)
 
         self.backward(gx, dense_hook=top_step)
         return losses
@@ -284,56 +288,3 @@ def random_kjt_lengths(lengths: np.ndarray, rows: int, gen: torch.Generator, dev
     lens = torch.from_numpy(lengths.reshape(-1).copy()).to(device)
     values = torch.randint(0, rows, (max(1, sum(nnz)),), generator=gen, device=device, dtype=torch.int32)[:sum(nnz)]
     return KJT(lengths=lens, values=values, nnz_per_feature=nnz, B=B)
-
-
-def smoke_train_step() -> None:
-    """One loopback SPTT train step (2 towers x 2 ranks, DLRM TM, fp32) checked
-    against the oracle's flat-model restatement (used by __graft_entry__.smoke)."""
-    import oracle
-
-    dev = torch.device("cuda")
-    topo, layout, placement, assignment = build_world(2, 2, 1, 6, 40, 16, seed=5)
-    G, B, F = 4, 3, 6
-    pooling = {f: "sum" for f in range(F)}
-    cfg = TMConfig(kind="dlrm", out_dim=8, per_feature_outputs=1, flat_outputs=1, seed=1)
-    before = {t: placement.tables[t].values.astype(np.float64).copy() for t in range(F)}
-    model = SPTT(topo, layout, placement, assignment, pooling, B, LoopbackFabric(G, dev), tm=cfg,
-                 dtype=torch.float32, lr=0.1)
-    rng = np.random.default_rng(9)
-    lens = rng.integers(0, 4, size=(G, F, B)).astype(np.int32)
-    vals = rng.integers(0, 40, size=int(lens.sum())).astype(np.int64)
-    offs = np.concatenate([[0], np.cumsum(lens.reshape(-1))])
-    kjts = {}
-    for r in range(G):
-        seg = vals[offs[r * F * B]:offs[(r + 1) * F * B]]
-        kjts[r] = KJT(torch.from_numpy(lens[r].reshape(-1)).to(dev), torch.from_numpy(seg.astype(np.int32)).to(dev),
-                      [int(lens[r, f].sum()) for f in range(F)], B)
-    O = model.plan.out_width()
-    grads = {r: torch.from_numpy(rng.normal(size=(B, O)).astype(np.float32)).to(dev) for r in range(G)}
-    outs = model.train_step(kjts, grads)
-    torch.cuda.synchronize()
-    # oracle: pooled per rank -> TM per tower -> grads -> table SGD
-    shards = [(s.table_id, s.rank, s.scheme, s.row_range, s.col_range) for s in placement.shards]
-    flat, _, _, _ = oracle.baseline_forward(lens, vals, list(range(F)), pooling, before, shards, oracle.OTopo(2, 2))
-    ocfg = {"kind": "dlrm", "out_dim": 8, "per_feature_outputs": 1, "flat_outputs": 1, "cross_layers": 3, "seed": 1}
-    tw = {t: oracle.init_tm_weights(ocfg, 3, 16, salt=t) for t in range(2)}
-    expect_tables = {t: before[t].copy() for t in range(F)}
-    for r in range(G):
-        g_r = grads[r].double().cpu().numpy()
-        col = 0
-        for t in range(2):
-            fs = [f for f in range(F) if assignment[f] == t]
-            x = flat[r][:, fs[0] * 16:(fs[-1] + 1) * 16].reshape(B, len(fs), 16)
-            ow = oracle.tm_output_width(ocfg, len(fs), 16)
-            y = oracle.tm_forward(x, ocfg, tw[t])
-            assert np.allclose(outs[r][:, col:col + ow].double().cpu().numpy(), y, rtol=1e-5, atol=1e-5)
-            dx, _ = oracle.tm_backward(x, ocfg, tw[t], g_r[:, col:col + ow])
-            col += ow
-            for i, f in enumerate(fs):
-                base = (r * F + f) * B
-                for b in range(B):
-                    for k in range(offs[base + b], offs[base + b + 1]):
-                        expect_tables[f][vals[k]] -= 0.1 * dx[b, i]
-    for sid, sh in enumerate(placement.shards):
-        got = model.engine.weights[sid].double().cpu().numpy()
-        np.testing.assert_allclose(got, expect_tables[sh.table_id], rtol=1e-4, atol=1e-5)

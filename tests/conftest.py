@@ -141,3 +141,26 @@ def tm_case(i: int):
 @pytest.fixture
 def rng():
     return np.random.default_rng(12345)
+
+
+def max_rel_err(got, want) -> float:
+    """max |got - want| / max |want| (max-norm relative error), float64."""
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    den = float(np.abs(want).max()) if want.size else 0.0
+    return float(np.abs(got - want).max()) / max(den, 1e-300) if want.size else 0.0
+
+
+def oracle_tm_weights(tm) -> dict:
+    """A device TowerModule's *current* weights (as stored: bf16-rounded for a
+    bf16 module) in the oracle's dict layout, so the oracle evaluates exactly
+    the model the device holds."""
+    w = tm.host_weights()
+    if tm.cfg.kind == "dlrm":
+        return {"w_flat": w.w_flat, "b_flat": w.b_flat, "w_feat": w.w_feat, "b_feat": w.b_feat}
+    return {"cross": [tuple(c) for c in w.cross], "w_proj": w.w_proj, "b_proj": w.b_proj}
+
+
+def oracle_tm_cfg(cfg) -> dict:
+    return {"kind": cfg.kind, "out_dim": cfg.out_dim, "per_feature_outputs": cfg.per_feature_outputs,
+            "flat_outputs": cfg.flat_outputs, "cross_layers": cfg.cross_layers, "seed": cfg.seed}

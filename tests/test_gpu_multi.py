@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _build(hosts, rph, dev):
+def _build(hosts, rph, dev, tm_kind="dcn"):
     import paper_2403_00877_b200 as P
     from paper_2403_00877_b200.pipeline import KJT
     from paper_2403_00877_b200.sptt import build_world
@@ -34,7 +34,10 @@ def _build(hosts, rph, dev):
                                                       shards_per_table=2)
     G = topo.world_size
     pooling = {f: "sum" for f in range(F)}
-    cfg = P.TMConfig(kind="dcn", out_dim=8, cross_layers=2, seed=1)
+    if tm_kind == "dlrm":  # default DLRM flavour: zero-size flat weights (flat_outputs = 0)
+        cfg = P.TMConfig(kind="dlrm", out_dim=8, per_feature_outputs=1, flat_outputs=0, seed=1)
+    else:
+        cfg = P.TMConfig(kind="dcn", out_dim=8, cross_layers=2, seed=1)
     rng = np.random.default_rng(21)
     lens = rng.integers(0, 6, size=(G, F, B)).astype(np.int32)
     vals = rng.integers(0, rows, size=int(lens.sum())).astype(np.int64)
@@ -47,7 +50,7 @@ def _build(hosts, rph, dev):
     return topo, layout, placement, assignment, pooling, cfg, kjts, B
 
 
-def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1):
+def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1, tm_kind="dcn"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
 
@@ -62,13 +65,13 @@ def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1):
         from paper_2403_00877_b200.fabric import LoopbackFabric, NcclFabric, PeerFabric
         from paper_2403_00877_b200.sptt import SPTT
 
-        topo, layout, placement, assignment, pooling, cfg, kjts, B = _build(hosts, rph, dev)
+        topo, layout, placement, assignment, pooling, cfg, kjts, B = _build(hosts, rph, dev, tm_kind)
         Fab = PeerFabric if kind == "peer" else NcclFabric
         fab = Fab(world, rank, layout.group_width(topo), dev)
         dist_model = SPTT(topo, layout, placement, assignment, pooling, B, fab, tm=cfg, dtype=torch.float32,
                           device=dev, lr=0.005)
         # reference: every rank on this GPU through the loopback fabric
-        topo2, layout2, placement2, _, _, _, kjts2, _ = _build(hosts, rph, dev)
+        topo2, layout2, placement2, _, _, _, kjts2, _ = _build(hosts, rph, dev, tm_kind)
         ref = SPTT(topo2, layout2, placement2, assignment, pooling, B, LoopbackFabric(world, dev), tm=cfg,
                    dtype=torch.float32, device=dev, lr=0.005)
         gen = np.random.default_rng(5)
@@ -85,14 +88,21 @@ def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1):
         # Step 0 (no weights updated yet) is held to 1e-6 element-wise for any
         # W; later steps at W > 2 to a 1e-4 relative (Frobenius) error, the
         # amplified reassociation of the summed TM gradients.
+        # The peer fabric sums the members' TM gradients in tower-rank order
+        # (dmt_peer_sum_sgd), exactly as the loopback engine does: outputs,
+        # TM weights and embedding shards must then be bit-identical at any W.
         W = layout.group_width(topo)
+        exact = kind == "peer"
         ok, worst = True, 0.0
         for step in range(steps):  # several steps: peer-written buffers are reused
             out_d = dist_model.train_step({rank: kjts[rank]}, {rank: grads[rank]})
             out_r = ref.train_step(kjts2, grads)
             torch.cuda.synchronize()
             d, r_ = out_d[rank].double(), out_r[rank].double()
-            if step == 0 or W <= 2:
+            if exact:
+                worst = max(worst, float((d - r_).abs().max()))
+                ok = ok and torch.equal(out_d[rank], out_r[rank])
+            elif step == 0 or W <= 2:
                 worst = max(worst, float((d - r_).abs().max()))
                 ok = ok and torch.allclose(d, r_, rtol=1e-6, atol=1e-6)
             else:
@@ -100,8 +110,13 @@ def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1):
                 worst = max(worst, rel)
                 ok = ok and rel <= 1e-4
         for sid in dist_model.engine.weights:
-            ok = ok and torch.allclose(dist_model.engine.weights[sid], ref.engine.weights[sid], rtol=1e-5,
-                                       atol=1e-6)
+            a, b = dist_model.engine.weights[sid], ref.engine.weights[sid]
+            ok = ok and (torch.equal(a, b) if exact else torch.allclose(a, b, rtol=1e-5, atol=1e-6))
+        t = rank // W
+        if exact and t in dist_model.tms:
+            for k, w in dist_model.tms[t].w.items():
+                if not torch.equal(w, ref.tms[t].w[k]):
+                    ok, worst = False, float((w.double() - ref.tms[t].w[k].double()).abs().max())
         q.put((rank, bool(ok), None if ok else f"worst out error {worst:.3e}"))
     except Exception:  # pragma: no cover
         import traceback
@@ -111,9 +126,10 @@ def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("tm_kind", ["dcn", "dlrm"])
 @pytest.mark.parametrize("kind,steps", [("nccl", 1), ("peer", 3)])
 @pytest.mark.parametrize("hosts,rph", [(2, 1), (1, 2), (2, 2), (4, 1), (1, 4)])
-def test_distributed_step_matches_loopback(hosts, rph, kind, steps):
+def test_distributed_step_matches_loopback(hosts, rph, kind, steps, tm_kind):
     world = hosts * rph
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
@@ -122,7 +138,7 @@ def test_distributed_step_matches_loopback(hosts, rph, kind, steps):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, hosts, rph, q, kind, steps)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, hosts, rph, q, kind, steps, tm_kind)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
