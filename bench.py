@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling runs)")
     ap.add_argument("--cpu-sample", type=int, default=256, help="samples per CPU-baseline step")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1 reference-API legs")
+    ap.add_argument("--lr", type=float, default=1e-2, help="embedding (sparse) learning rate")
+    ap.add_argument("--dense-lr", type=float, default=1e-4, help="tower-module / head learning rate")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 C2 record at N=1")
     return ap.parse_args()
 
@@ -393,7 +395,7 @@ def main():
             topo, layout, placement, assignment = device_world(T, W, 1, F, args.rows, Nd, dtype, [rank], seed=0,
                                                                device=dev)
             self.model = SPTT(topo, layout, placement, assignment, pooling, B, fabric, tm=tm_cfg, dtype=dtype,
-                              device=dev, mode=mode, lr=1e-2, dense_lr=1e-4, top=top_cfg)
+                              device=dev, mode=mode, lr=args.lr, dense_lr=args.dense_lr, top=top_cfg)
             gen = torch.Generator(device=dev).manual_seed(1234 + rank)
             if args.pool_dist == "powerlaw":
                 from paper_2403_00877_b200.sptt import powerlaw_lengths, random_kjt_lengths
@@ -531,7 +533,8 @@ def main():
             src, graph_ok, err = "eager", True, None
             if clocks is not None:
                 clocks.start()
-            gtimers = PhaseTimers(external=True)
+            # the events are graph nodes: they must live as long as the graph
+            gtimers = self.gtimers = PhaseTimers(external=True)
             try:
                 if args.pool_dist != "fixed":
                     raise RuntimeError("ragged per-batch nnz: eager steps (step-a counts exchange per batch)")

@@ -234,8 +234,10 @@ enum dmt_gemm_flags {
   /* tuning overrides (benchmarks): no L2 prefetch of the epilogue operands;
    * force the tile width BN = 64 * ((flags & BN_MASK) >> BN_SHIFT) */
   DMT_GEMM_NO_PREFETCH = 16,
-  /* opt-in: 2-CTA clusters sharing each B tile (TMA multicast) */
+  /* force / forbid cta_group::2 pairs (256 x BN tiles, B split across the
+   * pair); default: pairs for BN 256 tiles of wide outputs (n >= 2048) */
   DMT_GEMM_CLUSTER = 32,
+  DMT_GEMM_SINGLE_CTA = 64,
   DMT_GEMM_BN_SHIFT = 8,
   DMT_GEMM_BN_MASK = 0xF00
 };

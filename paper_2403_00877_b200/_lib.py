@@ -20,7 +20,7 @@ DT_F32, DT_BF16, DT_F64, DT_F16 = 0, 1, 2, 3
 POOL_NONE, POOL_SUM, POOL_MEAN = 0, 1, 2
 EPI_NONE, EPI_BIAS, EPI_CROSS, EPI_ACC, EPI_DCN_BWD, EPI_DCN_FINAL = 0, 1, 2, 3, 4, 5
 GEMM_TRANS_A, GEMM_TRANS_B, GEMM_AUX2_ACCUM, GEMM_SCALE_ACC = 1, 2, 4, 8
-GEMM_NO_PREFETCH, GEMM_BN_SHIFT, GEMM_CLUSTER = 16, 8, 32  # tuning overrides (benchmarks only)
+GEMM_NO_PREFETCH, GEMM_BN_SHIFT, GEMM_CLUSTER, GEMM_SINGLE_CTA = 16, 8, 32, 64  # tuning overrides
 GEMM_MAX_PAIRS = 4
 MAX_PEER_SRCS = 8  # DMT_MAX_PEER_SRCS (include/dmt.h)
 OPT_SGD, OPT_ROWWISE_ADAGRAD = 0, 1

@@ -115,6 +115,43 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t b
   }
 }
 
+// cta_group::2: the leader CTA issues one MMA for the pair (M = 256: each CTA
+// supplies 128 rows of A and half of B's columns from its own shared memory at
+// the same offsets; each CTA's TMEM receives its own 128 accumulator rows)
+__device__ __forceinline__ void umma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                      uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// completion of the pair's MMAs -> the barrier at this offset in every CTA of mask
+__device__ __forceinline__ void umma2_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// shared::cluster address of the same shared variable in CTA ``rank``
+__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA into this CTA's shared memory, completing tx bytes on the leader CTA's barrier
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -210,6 +247,17 @@ struct Operand {
 #pragma unroll
       for (int c = 0; c < ROWS / ATOM; ++c)
         if ((c & 1) == rank) tma_load_2d_mc(dst + c * COL_BYTES, map, bar, r0 + c * ATOM, k0, 0x3);
+    }
+  }
+  // 2-SM pair: ROWS rows starting at r0 into this CTA, tx on the leader's barrier
+  template <int ROWS>
+  __device__ static __forceinline__ void load_2sm(uint8_t* dst, const CUtensorMap* map, uint32_t leader_bar, int k0,
+                                                  int r0) {
+    if constexpr (!MN) {
+      tma_load_2d_2sm(dst, map, leader_bar, k0, r0);
+    } else {
+#pragma unroll
+      for (int c = 0; c < ROWS / ATOM; ++c) tma_load_2d_2sm(dst + c * COL_BYTES, map, leader_bar, r0 + c * ATOM, k0);
     }
   }
   template <int ROWS>
@@ -547,8 +595,12 @@ __device__ __forceinline__ void colsum_chunk(const Params& p, float* stile, int6
 // BN: tile N (64/128/256); NOPS: 1 (plain) or 3 (3xTF32); KIND: 0 f16-family, 1 tf32
 // FEAT: compile in the DCN-backward extras (fused bias-gradient column sums,
 // DCN_FINAL pair sums); kept out of the other variants' register budget.
-// CL: CTAs per cluster along M (1, or 2 = the pair shares each B tile: both
-// CTAs load half and multicast it, halving B's L2 -> SM traffic).
+// CL: CTAs per cluster along M: 1, or 2 = a cta_group::2 pair.  The pair
+// computes a 256 x BN tile with one MMA stream issued by the leader CTA: each
+// CTA stages its own 128 rows of A and one half of B's BN columns, so every
+// operand byte is read from shared memory once for the pair (a single-CTA
+// 128 x BN tile re-reads all of B per CTA: 1.5x the shared-memory operand
+// traffic at BN = 256, which the epilogue's staging then competes with).
 template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, bool AMN, bool BMN, bool FEAT,
           int CL = 1>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -556,7 +608,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_lo,
             const __grid_constant__ EpiMaps emaps, const Params p, uint32_t idesc) {
   constexpr int A_BYTES = kBlockM * kAtomBytes;
-  constexpr int B_BYTES = BN * kAtomBytes;
+  constexpr int B_BYTES = (BN / CL) * kAtomBytes;  // this CTA's share of the B tile
+  static_assert(CL == 1 || (KIND == 0 && NOPS == 1), "2-SM pairs: 16-bit operands");
   constexpr int NSETS = (NOPS == 3) ? 2 : 1;  // hi (+ lo) operand copies
   constexpr int STAGE_BYTES = NSETS * (A_BYTES + B_BYTES);
   // tf32 (fp32 parity path): two accumulators + two chunk-scratch buffers
@@ -579,7 +632,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tiles_m = ceil_div(p.m, kBlockM), tiles_n = ceil_div(p.n, BN);
   // work unit = CL vertically adjacent tiles sharing n0 (one per cluster CTA)
-  const int64_t num_units = (tiles_m / CL) * tiles_n;
+  const int64_t num_units = ceil_div(tiles_m, CL) * tiles_n;
   const int crank = CL > 1 ? (int)cluster_rank() : 0;
   const int64_t u_first = blockIdx.x / CL, u_step = gridDim.x / CL;
   auto unit_m0 = [&](int64_t u) { return (int64_t)(((u / tiles_n) * CL + crank) * kBlockM); };
@@ -591,22 +644,29 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);  // released by every cluster CTA's MMA warp
+      mbar_init(&full[s], 1);   // (pair: only the leader's is used; both CTAs' TMA complete on it)
+      mbar_init(&empty[s], 1);  // released by the (leader's) MMA commit
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], kEpiWarps);  // one arrive per epilogue warp
+      mbar_init(&tempty[s], kEpiWarps * CL);  // one arrive per epilogue warp of the pair (leader's)
       mbar_init(&sfull[s], 1);
       mbar_init(&sempty[s], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CL == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   if constexpr (CL > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
@@ -636,10 +696,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
-          OA::template load<kBlockM>(sa, &map_a, &full[stage], kb * K_ELEMS, m0);
-          if constexpr (CL > 1) OB::template load_half_mc<BN>(sb, &map_b, &full[stage], kb * K_ELEMS, n0, crank);
-          else OB::template load<BN>(sb, &map_b, &full[stage], kb * K_ELEMS, n0);
+          if constexpr (CL == 2) {
+            // both CTAs' loads complete on the leader's barrier; the leader
+            // expects the pair's bytes
+            if (crank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+            const uint32_t lbar = mapa_rank(&full[stage], 0);
+            OA::template load_2sm<kBlockM>(sa, &map_a, lbar, kb * K_ELEMS, m0);
+            OB::template load_2sm<BN / 2>(sb, &map_b, lbar, kb * K_ELEMS, n0 + crank * (BN / 2));
+          } else {
+            mbar_expect_tx(&full[stage], STAGE_BYTES);
+            OA::template load<kBlockM>(sa, &map_a, &full[stage], kb * K_ELEMS, m0);
+            OB::template load<BN>(sb, &map_b, &full[stage], kb * K_ELEMS, n0);
+          }
           if constexpr (NSETS == 2) {
             uint8_t* sa2 = sb + B_BYTES;
             uint8_t* sb2 = sa2 + A_BYTES;
@@ -653,7 +721,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && crank == 0) {  // a pair's MMAs are issued by its leader
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -692,7 +760,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           for (int kk = 0; kk < kAtomBytes / kUmmaKBytes; ++kk) {
             const uint64_t ada = OA::kstep(kk), adb = OB::kstep(kk);
             const uint32_t accum = (first && kk == 0) ? 0u : 1u;
-            umma<KIND>(tmem_t, da + ada, db + adb, idesc, accum);
+            if constexpr (CL == 2) umma2(tmem_t, da + ada, db + adb, idesc, accum);
+            else umma<KIND>(tmem_t, da + ada, db + adb, idesc, accum);
             if constexpr (NSETS == 2) {
               uint8_t* sa2 = sb + B_BYTES;
               uint8_t* sb2 = sa2 + A_BYTES;
@@ -702,9 +771,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
               umma<KIND>(tmem_t, da2 + ada, db + adb, idesc, 1u);  // lo * hi
             }
           }
-          // smem slot reusable once these MMAs retire (in every cluster CTA:
-          // the peer multicasts into this slot too)
-          if constexpr (CL > 1) umma_commit_mc(&empty[stage], 0x3);
+          // smem slot reusable once these MMAs retire (in both CTAs of a pair)
+          if constexpr (CL == 2) umma2_commit_mc(&empty[stage], 0x3);
           else umma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           first = false;
@@ -712,7 +780,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         if constexpr (KIND == 1) {
           if (tmem_t != tmem_d) umma_commit(&sfull[(s_it - 1) & 1]);
         }
-        umma_commit(&tfull[acc]);  // accumulator complete
+        if constexpr (CL == 2) umma2_commit_mc(&tfull[acc], 0x3);  // both CTAs' accumulators complete
+        else umma_commit(&tfull[acc]);  // accumulator complete
       }
     }
   } else {
@@ -813,7 +882,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
         __syncwarp();
         tc_fence_before();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if constexpr (CL == 2) mbar_arrive_cluster(mapa_rank(&tempty[acc], 0));
+          else mbar_arrive(&tempty[acc]);
+        }
         continue;
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -976,17 +1048,27 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CL == 2) mbar_arrive_cluster(mapa_rank(&tempty[acc], 0));
+        else mbar_arrive(&tempty[acc]);
+      }
     }
   }
 
   __syncthreads();
-  if (warp == 1) {
+  if constexpr (CL == 2) {
+    // both CTAs done with the pair's TMEM and barriers before the dealloc /
+    // exit (the peer's epilogue arrives on the leader's barriers)
+    cluster_sync_all();
+    if (warp == 1) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
+    }
+  } else if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
   }
-  // no CTA may exit while its peer can still multicast into it / arrive on it
-  if constexpr (CL > 1) cluster_sync_all();
 }
 
 // ---------------------------------------------------------------- host ------
@@ -1071,7 +1153,7 @@ template <int BN, int NOPS, int KIND, int STAGES, typename TIN, typename TO, boo
           int CL = 1>
 static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cudaStream_t s) {
   constexpr int NSETS = (NOPS == 3) ? 2 : 1;
-  constexpr int STAGE_BYTES = NSETS * (kBlockM + BN) * kAtomBytes;
+  constexpr int STAGE_BYTES = NSETS * (kBlockM + BN / CL) * kAtomBytes;
   constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
                           (size_t)kEpiWarps * kStileFloats * 4 /*epilogue staging*/;
   static_assert(SMEM <= 232448, "smem");
@@ -1154,7 +1236,7 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   }
   int64_t tiles = ceil_div(a->m, kBlockM) * ceil_div(a->n, BN);
   const int fmt = (KIND == 1) ? 2 : (std::is_same<TIN, __half>::value ? 0 : 1);
-  uint32_t idesc = make_idesc(fmt, kBlockM, BN, AMN, BMN);
+  uint32_t idesc = make_idesc(fmt, kBlockM * CL, BN, AMN, BMN);  // pair: M = 256
   if constexpr (CL == 1) {
     int grid = (int)std::min<int64_t>(tiles, DMT_NUM_SMS);
     kern<<<grid, kThreads, SMEM, s>>>(ma, mb, mal, mbl, em, p, idesc);
@@ -1179,7 +1261,7 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
       if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = DMT_NUM_SMS / CL;
       max_clusters = n;
     }
-    const int64_t units = tiles / CL;
+    const int64_t units = ceil_div(a->m, (int64_t)kBlockM * CL) * ceil_div(a->n, (int64_t)BN);
     cfg.gridDim = dim3((unsigned)(std::min<int64_t>(units, max_clusters) * CL));
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mal, mbl, em, p, idesc);
     if (e != cudaSuccess) {
@@ -1229,14 +1311,18 @@ static int dispatch_n(const dmt_gemm_args* a, const void* alo, const void* blo, 
   } else {
     const int bn = pick_bn(a->m, a->n, a->flags);
     if constexpr (std::is_same<TIN, __nv_bfloat16>::value && !FEAT) {
-      // 2-CTA clusters sharing B (multicast), opt-in: parity-green, but it
-      // measured equal to the single-CTA kernel (the mainloop is not bound by
-      // L2 -> SM operand traffic), so the default stays single-CTA
-      const bool pair = (a->flags & DMT_GEMM_CLUSTER) && (ceil_div(a->m, kBlockM) % 2 == 0) &&
-                        (bn == 256 || bn == 192) && ceil_div(a->m, kBlockM) * ceil_div(a->n, (int64_t)bn) >= 2 * 148;
+      // cta_group::2 pairs (256 x BN tiles; each CTA holds half of B): BN 256,
+      // or 192 with K-major B (an MN-major half must be whole 64-column atoms)
+      // Measured (tools/gemm_bench.py, B200): pairs win on the 3328-wide T = 1
+      // tower GEMMs (dW 190 -> 144-155 us, fused-SGD dW 164 -> 142, crossnet
+      // 156 -> 148, DCN_BWD 183 -> 172) and are neutral or slower on the
+      // 1664-wide ones, where the tile-width choice is BN 192.
+      const bool pair_ok = (bn == 256 || (bn == 192 && !BMN)) && ceil_div(a->m, kBlockM) >= 2;
+      const bool pair = pair_ok && !(a->flags & DMT_GEMM_SINGLE_CTA) &&
+                        ((a->flags & DMT_GEMM_CLUSTER) || (bn == 256 && a->n >= 2048));
       if (pair) {
-        if (bn == 256) return launch<256, 1, 0, 4, TIN, TO, AMN, BMN, FEAT, 2>(a, alo, blo, s);
-        return launch<192, 1, 0, 4, TIN, TO, AMN, BMN, FEAT, 2>(a, alo, blo, s);
+        if (bn == 256) return launch<256, 1, 0, 5, TIN, TO, AMN, BMN, FEAT, 2>(a, alo, blo, s);
+        if constexpr (!BMN) return launch<192, 1, 0, 6, TIN, TO, AMN, BMN, FEAT, 2>(a, alo, blo, s);
       }
     }
     switch (bn) {

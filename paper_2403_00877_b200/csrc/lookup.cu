@@ -1234,12 +1234,16 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
   }
   if (max_b == 0) return DMT_OK;
   // apply variants (DMT_BWD_VARIANT, read once so prepare and apply agree):
-  // 0 (default) bucketed sort + apply; 2 the earlier register kernel over a
-  // CUB radix sort (one occurrence per group, 4 CTAs / SM); 1 its
-  // two-occurrence form; 4 the bulk-copy staged kernel -- all parity-tested
+  // 2 (default) register kernel over a CUB radix sort (one occurrence per
+  // group, 4 CTAs / SM); 1 its two-occurrence form; 4 the bulk-copy staged
+  // kernel; 0 the bucketed sort + apply (hand-written bucket scatter, shared-
+  // memory bitonic sort per bucket fused with the update) -- all
+  // parity-tested.  The bucketed form measured slower at C2 bf16 (apply 0.83
+  // vs 0.61 ms; its prepare's bucket-counter atomics 0.19 + 0.14 ms vs the CUB
+  // sort), so it is not the default.
   static const int bwd_variant = [] {
     const char* e = getenv("DMT_BWD_VARIANT");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 2;
   }();
   // fast path: no mean pooling, 16-byte aligned gradient rows inside one
   // buffer (offset < 32 GB), <= kMaxShards distinct shards, vector widths

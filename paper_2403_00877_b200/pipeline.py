@@ -21,6 +21,7 @@ Reference: towersim/exchange.py:149-462 (forward only; the backward is new).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -388,21 +389,18 @@ class SpttEngine:
         err = torch.zeros(1, dtype=torch.int32, device=dev) if check_indices else None
         for r in self.local:
             offsets = K.lengths_to_offsets(recv_len[r][: p.owner_bags(r)])
+            nnz = sum(recv_val_splits[r])
+            if save and self._prepare_with_lookup:
+                self._launch_prepare(r, offsets, recv_val[r], nnz)
             with self._t("lookup_fwd"):
                 table = self.seg_fwd_p2p if self.p2p_d else self.seg_fwd[r]
                 K.pooled_lookup_fwd(table, offsets, recv_val[r], err)
-            nnz = sum(recv_val_splits[r])
             self._owner[r] = (offsets, recv_val[r], nnz)
-            if save:
+            if save and not self._prepare_with_lookup:
                 # the embedding backward's key build + radix sort need only the
                 # indices: run them on a side stream, overlapped with the tower
                 # module forward/backward and the exchanges (joined in backward)
-                side = self._side_stream()
-                side.wait_stream(torch.cuda.current_stream())
-                with torch.cuda.stream(side):
-                    K.pooled_lookup_bwd_prepare(self.seg_bwd[r], offsets, recv_val[r], nnz, self.key_space[r],
-                                                self._bwd_workspace(r, nnz))
-                self._prepared[r] = True
+                self._launch_prepare(r, offsets, recv_val[r], nnz)
         if err is not None:
             K.raise_lookup_errors(err)
         if self.mode == "flat":
@@ -672,7 +670,24 @@ class SpttEngine:
         else:
             self.overlap_with_embedding_update(dense_hook, lr, optimizer, eps)
 
+    # DMT_PREPARE_INLINE=1: run the embedding-backward prepare (keys + sort)
+    # on the launching stream instead of overlapping it with the tower module;
+    # DMT_PREPARE_AT=lookup: fork it before the lookup so it overlaps the
+    # (HBM-bound) lookup rather than the persistent tower-module GEMMs
+    _prepare_inline = os.environ.get("DMT_PREPARE_INLINE", "0") == "1"
+    _prepare_with_lookup = os.environ.get("DMT_PREPARE_AT", "tm") == "lookup"
+
+    def _launch_prepare(self, r, offsets, vals, nnz) -> None:
+        side = self._side_stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            K.pooled_lookup_bwd_prepare(self.seg_bwd[r], offsets, vals, nnz, self.key_space[r],
+                                        self._bwd_workspace(r, nnz))
+        self._prepared[r] = True
+
     def _side_stream(self):
+        if self._prepare_inline:
+            return torch.cuda.current_stream()
         if self._side is None:
             self._side = torch.cuda.Stream(device=self.device)
         return self._side
@@ -695,7 +710,8 @@ class SpttEngine:
             ws = self._bwd_workspace(r, nnz)
             with self._t("lookup_bwd"):
                 if self._prepared.get(r):
-                    torch.cuda.current_stream().wait_stream(self._side)
+                    if self._side is not None:
+                        torch.cuda.current_stream().wait_stream(self._side)
                     K.pooled_lookup_bwd_apply(self.seg_bwd[r], nnz, ks, optimizer, lr, eps, ws)
                 else:
                     K.pooled_lookup_bwd(self.seg_bwd[r], offsets, vals, nnz, ks, optimizer, lr, eps, ws)

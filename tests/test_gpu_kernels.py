@@ -214,27 +214,61 @@ def test_gemm_mn_major_operands(ta, tb, dt, m, n, k):
     assert (out.double() - want).abs().max().item() <= tol * scale
 
 
-@pytest.mark.parametrize("tb", [False, True])
-@pytest.mark.parametrize("m,n,k", [(8192, 1536, 256), (4096, 2560, 192)])
-def test_gemm_cluster_multicast_matches_single_cta(tb, m, n, k):
-    """Opt-in 2-CTA cluster variant (each CTA loads half of the B tile and
-    multicasts it): bit-identical to the single-CTA kernel (same MMA order)."""
+@pytest.mark.parametrize("epi", ["cross", "dcn_bwd", "dcn_final", "sgd", "plain_mn"])
+@pytest.mark.parametrize("m,n,k,bn", [(8192, 3328, 3328, 0), (16384, 1664, 1664, 0), (300, 512, 200, 4),
+                                      (4096, 2560, 192, 3), (1000, 200, 72, 4)])
+def test_gemm_cta_pair_matches_single_cta(epi, m, n, k, bn):
+    """cta_group::2 pairs (one 256 x BN MMA stream per CTA pair, each CTA
+    staging half of B) are bit-identical to the single-CTA kernel: same
+    per-element K order.  Covers the C2 shapes, an odd 128-row tile count
+    (the peer CTA's rows past m), BN 192 / 256, K-major and MN-major operands
+    and the CROSS / DCN_BWD / DCN_FINAL / fused-SGD epilogues."""
     from paper_2403_00877_b200 import _lib as L
     from paper_2403_00877_b200 import kernels as K
 
+    dt = torch.bfloat16
     g = torch.Generator(device="cuda").manual_seed(m + n + k)
-    A = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
-    Bm = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
-    b = Bm.t().contiguous() if tb else Bm
+    A = torch.randn(m, k, device="cuda", generator=g).to(dt)
+    Bm = (torch.randn(n, k, device="cuda", generator=g) / k ** 0.5).to(dt)
+    x0 = torch.randn(m, n, device="cuda", generator=g).to(dt)
+    u = torch.randn(m, n, device="cuda", generator=g).to(dt)
     bias = torch.randn(n, device="cuda", generator=g)
-    x0 = torch.randn(m, n, device="cuda", generator=g).to(torch.bfloat16)
+    flags0 = bn << L.GEMM_BN_SHIFT
     outs = []
-    for fl in (0, L.GEMM_CLUSTER):
-        o = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
-        K.gemm(A, b, o, trans_b=tb, bias=bias, epilogue=L.EPI_CROSS, x0=x0, xl=x0, tune_flags=fl)
-        outs.append(o)
+    for fl in (flags0 | L.GEMM_SINGLE_CTA, flags0 | L.GEMM_CLUSTER):
+        if epi == "cross":
+            o = torch.empty(m, n, device="cuda", dtype=dt)
+            aux = torch.empty(m, n, device="cuda", dtype=dt)
+            K.gemm(A, Bm, o, bias=bias, epilogue=L.EPI_CROSS, x0=x0, xl=u, aux=aux, tune_flags=fl)
+            outs.append((o, aux))
+        elif epi == "dcn_bwd":  # dX-side: B read MN-major
+            Bt = Bm.t().contiguous()
+            o = x0.clone()
+            gu = torch.empty(m, n, device="cuda", dtype=dt)
+            dx0 = torch.ones(m, n, device="cuda", dtype=torch.float32)
+            K.gemm(A, Bt, o, trans_b=True, epilogue=L.EPI_DCN_BWD, c=o, beta=1.0, x0=x0, xl=u, aux=gu, aux2=dx0,
+                   aux2_accum=True, tune_flags=fl)
+            outs.append((o, gu, dx0))
+        elif epi == "dcn_final":
+            Bt = Bm.t().contiguous()
+            o = torch.empty(m, n, device="cuda", dtype=dt)
+            dx0 = torch.randn(m, n, device="cuda", generator=torch.Generator(device="cuda").manual_seed(1))
+            K.gemm(A, Bt, o, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=x0, beta=1.0, aux2=dx0, tune_flags=fl)
+            outs.append((o,))
+        elif epi == "sgd":  # W -= lr * A^T B (MN-major A and B, K = m)
+            At = A[: min(m, 4096)]
+            Bk = x0[: min(m, 4096)]
+            W = torch.ones(k, n, device="cuda", dtype=dt)
+            K.gemm(At, Bk, W, trans_a=True, trans_b=True, epilogue=L.EPI_ACC, beta=1.0, alpha=-1e-3, tune_flags=fl)
+            outs.append((W,))
+        else:  # plain, fp32 out, MN-major A
+            At = A.t().contiguous()
+            o = torch.empty(m, n, device="cuda", dtype=torch.float32)
+            K.gemm(At, Bm, o, trans_a=True, tune_flags=fl)
+            outs.append((o,))
     torch.cuda.synchronize()
-    assert torch.equal(outs[0], outs[1])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("rows,cols", [(8192, 3328), (1000, 256), (77, 64), (3, 8), (4096, 100)])

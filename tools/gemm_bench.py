@@ -84,13 +84,17 @@ def main():
          lambda: K.gemm(gu, W, out, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=u, beta=1.0,
                         pairs=[(x0, u), (xl, u), (x0, xl)]), None),
         ("bwd dX plain (K,MN)", 2 * R * M * M, lambda: K.gemm(gu, W, out, trans_b=True), None),
+        ("bwd dW fused sgd", 2 * R * M * M,
+         lambda: K.gemm(gu, xl, W, trans_a=True, trans_b=True, epilogue=L.EPI_ACC, beta=1.0, alpha=-1e-9), None),
+        ("bwd dWp", 2 * R * M * P, lambda: K.gemm(gy, xl, torch.empty(P, M, device="cuda"), trans_a=True,
+                                                  trans_b=True), lambda: torch.matmul(gy.t(), xl)),
         ("bwd g proj dcn_bwd", 2 * R * M * P,
          lambda: K.gemm(gy, Wp, out, trans_b=True, epilogue=L.EPI_DCN_BWD, x0=x0, xl=u, aux=xl, aux2=dx0),
          lambda: torch.matmul(gy, Wp)),
     ]
-    variants = [("auto", 0), ("cl2", L.GEMM_CLUSTER), ("nopf", L.GEMM_NO_PREFETCH)] + [
+    variants = [("auto", 0), ("single", L.GEMM_SINGLE_CTA), ("pair", L.GEMM_CLUSTER)] + [
         (f"bn{64 * j}", j << L.GEMM_BN_SHIFT) for j in (3, 4)] + [
-        (f"bn{64 * j}cl", (j << L.GEMM_BN_SHIFT) | L.GEMM_CLUSTER) for j in (3, 4)]
+        (f"bn{64 * j}pr", (j << L.GEMM_BN_SHIFT) | L.GEMM_CLUSTER) for j in (3, 4)]
     for name, flops, fn, ref in cases:
         line = f"{name:22s}"
         for vname, fl in variants:
