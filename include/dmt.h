@@ -151,7 +151,12 @@ typedef struct dmt_assemble_block {
   int32_t width;
   int32_t nsrc;
   int32_t first_src; /* index into the src table */
-  int32_t pad_;
+  /* multi-source (summed) blocks: bit s set = source s starts a new inner
+   * partial sum; the result is ((s0 + s1 + ..) + (sk + ..) + ..) in fp64 --
+   * the row-wise reduce-scatter order (per-owner partial, then group order,
+   * towersim/exchange.py:380-395 + simnet.py:173-192).  0 = one flat sum in
+   * source order (exchange.py:112-127). */
+  uint32_t groups;
 } dmt_assemble_block;
 
 typedef struct dmt_src {

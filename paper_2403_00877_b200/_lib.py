@@ -41,7 +41,7 @@ class LookupSegment(C.Structure):
 
 
 class AssembleBlock(C.Structure):
-    _fields_ = [("dst_col", i64), ("width", i32), ("nsrc", i32), ("first_src", i32), ("pad_", i32)]
+    _fields_ = [("dst_col", i64), ("width", i32), ("nsrc", i32), ("first_src", i32), ("groups", C.c_uint32)]
 
 
 class Src(C.Structure):

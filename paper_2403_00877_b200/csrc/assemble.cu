@@ -40,17 +40,28 @@ assemble_kernel(const dmt_assemble_block* __restrict__ blocks, const dmt_src* __
         *reinterpret_cast<V*>(o) = *reinterpret_cast<const V*>(p);
       }
     } else {
-      double acc[VEC];
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) acc[e] = 0.0;
+      // fp64 sums; the first term of each (inner / outer) sum is copied, not
+      // added to 0 (numpy's `total = first.copy(); total += ...`), so the
+      // bits -- a -0.0 partial included -- match the reference
+      double acc[VEC], grp[VEC];
+      bool have_acc = false;
       for (int s = 0; s < blk.nsrc; ++s) {
         const dmt_src sx = srcs[blk.first_src + s];
         const T* p = reinterpret_cast<const T*>(sx.ptr) + r * sx.ld + c;
+        const bool new_group = s > 0 && ((blk.groups >> s) & 1u);
+        if (new_group) {
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) acc[e] += to_d<T>(p[e]);
+          for (int e = 0; e < VEC; ++e) acc[e] = have_acc ? acc[e] + grp[e] : grp[e];
+          have_acc = true;
+        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const double v = to_d<T>(p[e]);
+          grp[e] = (s == 0 || new_group) ? v : grp[e] + v;
+        }
       }
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) o[e] = from_d<T>(acc[e]);
+      for (int e = 0; e < VEC; ++e) o[e] = from_d<T>(have_acc ? acc[e] + grp[e] : grp[e]);
     }
   }
 }

@@ -45,8 +45,12 @@ class ExchangeOptions:
     """exchange.py:57-81.  swap_bc / omit_permute are result-invariant orderings
     of the same data movement; on the GPU the permute is always fused into the
     lookup epilogue (zero extra bytes), so both are accepted and change nothing.
-    rowwise_reducescatter only changes the step-d byte accounting (results are
-    identical, exchange.py:380-395)."""
+    rowwise_reducescatter switches the step-d combine of row-wise features to
+    the reference's reduce-scatter (exchange.py:380-395): the byte accounting
+    of simnet.reduce_scatter and its summation order -- each owner's shard
+    partials first, then the owners in group order (simnet.py:173-192) -- which
+    can differ in the last bit from the row-range order of the all-to-all form
+    on real-valued tables."""
 
     swap_bc: bool = False
     omit_permute: bool = False

@@ -217,6 +217,7 @@ class Block:
     dst_col: int
     width: int
     srcs: list  # [(tensor, element offset, ld)]
+    groups: int = 0  # summed blocks: bit s = source s starts a new inner sum (dmt_assemble_block.groups)
 
 
 class AssembleTable:
@@ -230,7 +231,7 @@ class AssembleTable:
             if b.width == 0:
                 continue
             structs.append(L.AssembleBlock(dst_col=b.dst_col, width=b.width, nsrc=len(b.srcs),
-                                           first_src=len(srcs), pad_=0))
+                                           first_src=len(srcs), groups=b.groups))
             self.max_width = max(self.max_width, b.width)
             if b.width % vec or b.dst_col % vec:
                 vec_ok = False

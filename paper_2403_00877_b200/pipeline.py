@@ -170,7 +170,7 @@ class SpttEngine:
                 self.seg_fwd[r] = self._segments(r, b["send_x"])
                 self.seg_bwd[r] = self._segments(r, b["grad_x"], with_keys=True)
             if sptt:
-                self.asm_e[r] = self._assemble_table(p.e_blocks(r), b["recv_d"], b["X"], p.T * p.B)
+                self.asm_e[r] = self._assemble_table(p.e_blocks(r, rs=self.rs), b["recv_d"], b["X"], p.T * p.B)
                 blocks = [K.Block(col, w, [(b["recv_f"], off, w)]) for col, w, off in p.out_blocks_tower()]
                 self.asm_out[r] = K.AssembleTable(blocks, b["out"], p.B, dev)
             else:
@@ -324,7 +324,8 @@ class SpttEngine:
         blocks = []
         for fb in fblocks:
             if fb.rowwise:
-                blocks.append(K.Block(fb.dst_col, fb.width, [(src, pc.offset, pc.ld) for pc in fb.pieces]))
+                blocks.append(K.Block(fb.dst_col, fb.width, [(src, pc.offset, pc.ld) for pc in fb.pieces],
+                                      fb.groups))
             else:
                 for pc in fb.pieces:
                     blocks.append(K.Block(fb.dst_col + pc.c0, pc.width, [(src, pc.offset, pc.ld)]))

@@ -58,6 +58,7 @@ class FeatureBlock:
     width: int
     rowwise: bool
     pieces: tuple
+    groups: int = 0  # row-wise reduce-scatter order: bit s = piece s starts an owner's partial
 
 
 @dataclass
@@ -196,7 +197,11 @@ class ExchangePlan:
             off += self.T * self.B * self.SW[o]
         raise PlanError(f"owner {owner} not in rank {r}'s tower")
 
-    def _feature_blocks(self, feats, recv_offset) -> list[FeatureBlock]:
+    def _feature_blocks(self, feats, recv_offset, rs: bool = False) -> list[FeatureBlock]:
+        """``rs``: row-wise features combine in the reduce-scatter order of
+        exchange.py:380-395 -- each owner's shards summed in shard order, then
+        the owners' partials in group (rank) order (simnet.py:173-192) -- instead
+        of one sum in row-range order (_combine_pieces, exchange.py:112-127)."""
         blocks, col = [], 0
         for f in feats:
             sids = [sid for sid in self.live if self.shards[sid].table_id == f]
@@ -204,17 +209,27 @@ class ExchangePlan:
             if ROW_WISE in schemes and schemes != {ROW_WISE}:
                 raise PlanError("a table mixes row-wise and column-wise shards")
             rowwise = schemes == {ROW_WISE}
-            key = (lambda s: self.shards[s].row_range) if rowwise else (lambda s: self.shards[s].col_range)
-            pieces = []
-            for sid in sorted(sids, key=key):
+            if rowwise and rs:
+                key = lambda s: (self.shards[s].rank, s)
+            elif rowwise:
+                key = lambda s: self.shards[s].row_range
+            else:
+                key = lambda s: self.shards[s].col_range
+            pieces, groups, prev = [], 0, None
+            for j, sid in enumerate(sorted(sids, key=key)):
                 sh: Shard = self.shards[sid]
                 pieces.append(Piece(sid, recv_offset(sh.rank, self.k_of(sid)), sh.width,
                                     0 if rowwise else sh.col_range[0], sh.width))
-            blocks.append(FeatureBlock(f, col, self.dims[f], rowwise, tuple(pieces)))
+                if rowwise and rs and prev is not None and sh.rank != prev:
+                    groups |= 1 << j
+                prev = sh.rank
+            if groups and len(pieces) > 32:
+                raise PlanError("reduce-scatter order supports at most 32 row shards per table")
+            blocks.append(FeatureBlock(f, col, self.dims[f], rowwise, tuple(pieces), groups))
             col += self.dims[f]
         return blocks
 
-    def e_blocks(self, r: int) -> list[FeatureBlock]:
+    def e_blocks(self, r: int, rs: bool = False) -> list[FeatureBlock]:
         """Step-d assemble / step-e regroup into X (T*B, sum N) for member r."""
         return self._feature_blocks(self.tower_features[self.tower_of(r)],
                                     lambda o, k: self.d_recv_offset(r, o, k))

@@ -50,12 +50,13 @@ def golden_npz(name: str):
     return _cache[name]
 
 
-def acceptance_case(i: int):
-    """Rebuild the inputs of acceptance config i (tests/golden/make_golden.py)."""
+def acceptance_case(i: int, key: str = "acceptance"):
+    """Rebuild the inputs of acceptance config i (tests/golden/make_golden.py);
+    key "acceptance_real" = the 200-config sweep with real-valued tables."""
     from oracle import OTopo, integer_tables, uniform_tables
 
-    m = golden_meta()["acceptance"][i]
-    arr = golden_npz("acceptance")
+    m = golden_meta()[key][i]
+    arr = golden_npz(key)
     cfg = m["cfg"]
     t = cfg["tables"]
     shapes = {tid: (int(t["rows"]), int(t["dim"])) for tid in range(int(t["count"]))}
@@ -83,6 +84,27 @@ def acceptance_case(i: int):
         realigned=arr[f"c{i}_realigned"],
         exchange=cfg["exchange"],
     )
+
+
+def c1_full_inputs(TS, multi_hot: bool):
+    """Full-size C1 through a towersim-compatible API module ``TS`` (this
+    package): 2 x 4, 26 float64 U(-1, 1) tables x 100k x 64 (seed 0), B = 512,
+    batch seed 1 (tests/golden/make_golden.gen_c1_full)."""
+    topo = TS.ClusterTopology(2, 4)
+    layout = TS.TowerLayout(2)
+    tables = {t: TS.init_table_deterministic(t, 100_000, 64, seed=0) for t in range(26)}
+    assignment = {t: (0 if t < 13 else 1) for t in range(26)}
+    placement = TS.shard_tables(tables, {t: TS.TablePlan("table_wise", 1, assignment[t]) for t in tables}, topo,
+                                layout)
+    hot = (10, 30) if multi_hot else 1
+    batch = TS.make_batch(topo, tables, 512, {t: hot for t in tables}, seed=1)
+    return topo, placement, batch, TS.TowerPlan(layout, assignment), tables
+
+
+def sha256(a) -> str:
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
 def fp32_case(name: str):

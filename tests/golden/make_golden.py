@@ -112,11 +112,16 @@ def capture_step_a(fn, *args, **kwargs):
 # --------------------------------------------------------------------------- #
 # 1. the acceptance sweep (tests/test_acceptance.py:46-81): seed 2024, flags
 # --------------------------------------------------------------------------- #
-def gen_acceptance(n_configs: int = 60):
+def gen_acceptance(n_configs: int = 60, real_values: bool = False):
+    """``real_values``: the same configs with U(-1, 1) float64 tables (the
+    reference's own non-integer mode) instead of integer-valued ones, so sums
+    of row-wise partials exercise the reference's summation order bit for bit."""
     rng = np.random.default_rng(2024)
     meta, arrays = [], {}
     for i in range(n_configs):
         cfg = random_config(rng)
+        if real_values:
+            cfg["tables"]["integer_values"] = False
         swap, omit, rs = FLAG_COMBOS[i % len(FLAG_COMBOS)]
         cfg["exchange"] = {"swap_bc": swap, "omit_permute": omit, "rowwise_reducescatter": rs}
         ctx = RunContext(cfg)
@@ -154,6 +159,46 @@ def gen_acceptance(n_configs: int = 60):
             }
         )
     return meta, arrays
+
+
+# --------------------------------------------------------------------------- #
+# 1b. full-size C1: 2 x 4, F = 26, N = 64, B = 512 / rank, 100k
+# rows, float64 U(-1, 1) tables; single- and multi-hot.  The outputs are ~55 MB
+# per case, so the fixture keeps per-rank SHA-256 digests of the exact float64
+# bytes (plus the batch digest and a few rows) -- bit-exact checks at full size.
+# --------------------------------------------------------------------------- #
+def _sha(a: np.ndarray) -> str:
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def gen_c1_full():
+    out = {}
+    topo = ClusterTopology(2, 4)
+    layout = TowerLayout(2)
+    tables = {t: init_table_deterministic(t, 100_000, 64, seed=0) for t in range(26)}
+    assignment = {t: (0 if t < 13 else 1) for t in range(26)}
+    placement = shard_tables(tables, {t: TablePlan("table_wise", 1, assignment[t]) for t in tables}, topo, layout)
+    tp = TowerPlan(layout, assignment)
+    for name, hot in (("single_hot", 1), ("multi_hot", (10, 30))):
+        batch = make_batch(topo, tables, 512, {t: hot for t in tables}, seed=1)
+        tower = tower_exchange(batch, placement, tp, topo)
+        base = baseline_exchange(batch, placement, topo)
+        lengths, values = batch_to_kjt(batch)
+        out[name] = {
+            "hot": hot if hot == 1 else list(hot),
+            "lengths_sha": _sha(lengths.astype(np.int32)),
+            "values_sha": _sha(values.astype(np.int64)),
+            "nnz": int(values.size),
+            "tower_sha": {str(r): _sha(tower.outputs[r]) for r in range(8)},
+            "base_sha": {str(r): _sha(base.outputs[r]) for r in range(8)},
+            "tower_rows0_3": {str(r): tower.outputs[r][:4].tolist() for r in (0, 5)},
+            "tower_layout": layout_list(tower.layout),
+            "tower_trace": trace_table(tower.trace),
+            "base_trace": trace_table(base.trace),
+        }
+    return out
 
 
 # --------------------------------------------------------------------------- #
@@ -333,6 +378,13 @@ def main():
     acc_meta, acc_arr = gen_acceptance()
     meta["acceptance"] = acc_meta
     np.savez_compressed(os.path.join(HERE, "acceptance.npz"), **acc_arr)
+
+    # 200 configs of the acceptance sweep with real-valued tables
+    ar_meta, ar_arr = gen_acceptance(200, real_values=True)
+    meta["acceptance_real"] = ar_meta
+    np.savez_compressed(os.path.join(HERE, "acceptance_real.npz"), **ar_arr)
+
+    meta["c1_full"] = gen_c1_full()
 
     w_meta, w_arr = gen_worked_2x4()
     meta["worked_2x4"] = w_meta

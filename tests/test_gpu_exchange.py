@@ -11,6 +11,7 @@ from conftest import acceptance_case, fp32_case, golden_meta
 pytestmark = pytest.mark.gpu
 
 N_ACC = len(golden_meta()["acceptance"])
+N_ACC_REAL = len(golden_meta()["acceptance_real"])
 
 
 def _api_inputs(c, dtype=None):
@@ -37,9 +38,13 @@ def _api_inputs(c, dtype=None):
     return P, topo, layout, placement, batch, plan
 
 
-@pytest.mark.parametrize("i", range(N_ACC))
-def test_acceptance_configs_bit_exact(i):
-    c = acceptance_case(i)
+@pytest.mark.parametrize("key,i", [("acceptance", i) for i in range(N_ACC)] +
+                         [("acceptance_real", i) for i in range(N_ACC_REAL)])
+def test_acceptance_configs_bit_exact(key, i):
+    """The reference's acceptance sweep through the GPU API: 60 configs with
+    integer tables and 200 with real-valued float64 tables (bag-order lookup
+    sums, row-range and reduce-scatter combine orders all bit-exact)."""
+    c = acceptance_case(i, key)
     P, topo, layout, placement, batch, plan = _api_inputs(c)
     ex = c["exchange"]
     opts = P.ExchangeOptions(swap_bc=ex["swap_bc"], omit_permute=ex["omit_permute"],
@@ -101,3 +106,26 @@ def test_tm_forward_golden():
         weights = P.init_tm_weights(tc, m["F"], m["N"], salt=m["salt"])
         got = P.tm_forward(embs, tc, weights)
         np.testing.assert_allclose(got, out, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("multi", [False, True])
+def test_c1_full_size_bit_exact(multi):
+    """Full-size C1 (2 towers x 4, 26 x 100k x 64 float64 tables, B = 512 per
+    rank, single- and multi-hot) through tower_exchange / baseline_exchange on
+    the GPU: SHA-256 of every rank's exact float64 output equals the
+    reference's, and so do the step-a/d/f byte totals."""
+    import paper_2403_00877_b200 as P
+    from conftest import c1_full_inputs, sha256
+
+    m = golden_meta()["c1_full"]["multi_hot" if multi else "single_hot"]
+    topo, placement, batch, plan, _ = c1_full_inputs(P, multi)
+    tower = P.tower_exchange(batch, placement, plan, topo)
+    base = P.baseline_exchange(batch, placement, topo)
+    for r in range(8):
+        assert sha256(tower.outputs[r]) == m["tower_sha"][str(r)], r
+        assert sha256(base.outputs[r]) == m["base_sha"][str(r)], r
+    for r in ("0", "5"):
+        assert np.array_equal(tower.outputs[int(r)][:4], np.asarray(m["tower_rows0_3"][r]))
+    assert [list(b) for b in tower.layout.blocks] == m["tower_layout"]
+    for label in ("a", "d", "f"):
+        assert list(tower.trace.byte_totals(label)) == m["tower_trace"][label], label

@@ -31,6 +31,7 @@ from oracle import (
 )
 
 N_ACC = len(golden_meta()["acceptance"])
+N_ACC_REAL = len(golden_meta()["acceptance_real"])
 
 
 def _tm_cfg_from(m):
@@ -41,9 +42,13 @@ def _tm_cfg_from(m):
             "flat_outputs": t["flat_outputs"], "cross_layers": t["cross_layers"], "seed": t["seed"]}
 
 
-@pytest.mark.parametrize("i", range(N_ACC))
-def test_acceptance_config_bit_exact(i):
-    c = acceptance_case(i)
+@pytest.mark.parametrize("key,i", [("acceptance", i) for i in range(N_ACC)] +
+                         [("acceptance_real", i) for i in range(N_ACC_REAL)])
+def test_acceptance_config_bit_exact(key, i):
+    """Integer-valued tables (60 configs) and the 200-config sweep with
+    real-valued float64 tables, where every sum -- bag order, row-range order,
+    the reduce-scatter's per-owner then group order -- must match bit for bit."""
+    c = acceptance_case(i, key)
     topo = c["topo"]
     base, blayout, bwire, bflops = baseline_forward(
         c["lengths"], c["values"], c["features"], c["pooling"], c["tables"], c["shards"], topo)
@@ -199,3 +204,46 @@ def test_tm_input_grads_finite_difference(i):
     fd = (np.sum(g * tm_forward(embs + eps * v, cfg, w))
           - np.sum(g * tm_forward(embs - eps * v, cfg, w))) / (2 * eps)
     assert abs(fd - np.sum(dx * v)) <= 1e-6 * max(1.0, abs(fd))
+
+
+def test_acceptance_real_sweep_covers_rowwise_reducescatter():
+    """The real-valued sweep reaches the orders that integer tables cannot
+    distinguish: row-wise shards with and without the reduce-scatter form."""
+    ms = golden_meta()["acceptance_real"]
+    rw = [m for m in ms if m["cfg"]["tables"]["sharding"] == "row_wise"]
+    assert any(m["cfg"]["exchange"]["rowwise_reducescatter"] for m in rw)
+    assert any(not m["cfg"]["exchange"]["rowwise_reducescatter"] for m in rw)
+    assert not any(m["cfg"]["tables"]["integer_values"] for m in ms)
+
+
+@pytest.mark.parametrize("multi", [False, True])
+def test_c1_full_size_oracle_digests(multi):
+    """Full-size C1 (2 x 4, F = 26, N = 64, B = 512, 100k rows): the oracle's
+    float64 outputs hash to the reference's (SHA-256 of the exact bytes)."""
+    import paper_2403_00877_b200 as TS
+    from conftest import c1_full_inputs, sha256
+    from oracle import OTopo
+
+    m = golden_meta()["c1_full"]["multi_hot" if multi else "single_hot"]
+    topo, placement, batch, plan, tables = c1_full_inputs(TS, multi)
+    G, F, B = 8, 26, 512
+    lengths = np.zeros((G, F, B), dtype=np.int32)
+    vals = []
+    for r in range(G):
+        for f in range(F):
+            for b, bag in enumerate(batch.bags[r][f]):
+                lengths[r, f, b] = len(bag)
+                vals.extend(bag)
+    values = np.asarray(vals, dtype=np.int64)
+    assert sha256(lengths) == m["lengths_sha"] and sha256(values) == m["values_sha"]
+    shards = [(s.table_id, s.rank, s.scheme, s.row_range, s.col_range) for s in placement.shards]
+    tvals = {t: tables[t].values for t in tables}
+    pooling = dict(batch.pooling)
+    tower, tlayout, twire, _ = tower_forward(lengths, values, list(range(F)), pooling, tvals, shards,
+                                             {t: (0 if t < 13 else 1) for t in range(F)}, OTopo(2, 4))
+    base, _, _, _ = baseline_forward(lengths, values, list(range(F)), pooling, tvals, shards, OTopo(2, 4))
+    for r in range(G):
+        assert sha256(tower[r]) == m["tower_sha"][str(r)], r
+        assert sha256(base[r]) == m["base_sha"][str(r)], r
+    for label, entries in twire.items():
+        assert list(byte_totals(entries, OTopo(2, 4))) == m["tower_trace"][label], label
