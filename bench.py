@@ -47,6 +47,10 @@ def parse():
     ap.add_argument("--tm", default="dcn", choices=["dcn", "dlrm", "passthrough"])
     ap.add_argument("--tm-out", type=int, default=64)
     ap.add_argument("--cross-layers", type=int, default=3)
+    ap.add_argument("--model", default="dcn", choices=["dcn", "dlrm"],
+                    help="dcn: the DCN tower-module SPTT step (C2 / C4); dlrm: the C3 model -- DLRM (bottom MLP, "
+                         "dot interaction, top MLP, BCE) around SPTT with DLRM tower modules (c=1, p=0, D=--tm-out); "
+                         "the flat baseline interacts the full embeddings")
     ap.add_argument("--top", default="none", choices=["none", "dcn"],
                     help="full DCN + SPTT model: a data-parallel crossnet head to one logit + BCE loss on "
                          "synthetic labels (instead of a synthetic upstream gradient)")
@@ -274,7 +278,11 @@ def cpu_baseline(args) -> dict:
 
 def _config(args, N):
     T = _towers(args, N)
-    if args.pool_dist == "powerlaw":
+    if args.model == "dlrm":
+        wl = (f"C3-style DLRM + SPTT: {args.tables} tables x {args.rows} rows x dim {args.dim}, pooling {args.pool}, "
+              f"batch {args.batch}/GPU, DLRM tower modules D={args.tm_out}, 13 dense features, bottom 512-256-D, "
+              f"top 512-256-1, SPTT {T} x {N // T}")
+    elif args.pool_dist == "powerlaw":
         wl = (f"C5-style: {args.tables} tables x {args.rows} rows x dim {args.dim}, power-law pooling (mean "
               f"{args.pool}, max 200), batch {args.batch}/GPU, {args.tm} TM, SPTT {T} x {N // T}")
     elif N == 1:
@@ -284,7 +292,7 @@ def _config(args, N):
     return {"workload": wl,
             "tables": args.tables, "rows": args.rows, "dim": args.dim, "pooling_factor": args.pool,
             "batch_per_gpu": args.batch, "global_batch": args.batch * N, "tm": args.tm, "tm_out_dim": args.tm_out,
-            "cross_layers": args.cross_layers, "top": args.top, "towers": T, "gpus_per_tower": N // T, "optimizer": "sgd",
+            "cross_layers": args.cross_layers, "top": args.top, "model": args.model, "towers": T, "gpus_per_tower": N // T, "optimizer": "sgd",
             "pooling_dist": args.pool_dist,
             "parallelism": f"embedding model-parallel in tower, TM data-parallel in tower (T={T}, W={N // T})",
             "exchange": "loopback" if N == 1 else ("nvlink peer stores + barrier" if args.fabric == "peer"
@@ -371,6 +379,8 @@ def main():
         return (PeerFabric if kind == "peer" else NcclFabric)(N, rank, W, dev)
 
     fabric = make_fabric(args.fabric)
+    if args.model == "dlrm":
+        args.tm = "dlrm"
     tm_cfg = None if args.tm == "passthrough" else P.TMConfig(kind=args.tm, out_dim=args.tm_out, cross_layers=args.cross_layers,
                                                              per_feature_outputs=1, flat_outputs=0, seed=0)
     top_cfg = (P.TMConfig(kind="dcn", out_dim=1, cross_layers=args.cross_layers, seed=0) if args.top == "dcn"
@@ -394,8 +404,16 @@ def main():
             self.es = 2 if dtype == torch.bfloat16 else 4
             topo, layout, placement, assignment = device_world(T, W, 1, F, args.rows, Nd, dtype, [rank], seed=0,
                                                                device=dev)
-            self.model = SPTT(topo, layout, placement, assignment, pooling, B, fabric, tm=tm_cfg, dtype=dtype,
-                              device=dev, mode=mode, lr=args.lr, dense_lr=args.dense_lr, top=top_cfg)
+            dlrm = args.model == "dlrm"
+            self.model = SPTT(topo, layout, placement, assignment, pooling, B, fabric,
+                              tm=(None if dlrm and mode == "flat" else tm_cfg), dtype=dtype,
+                              device=dev, mode=mode, lr=args.lr, dense_lr=args.dense_lr,
+                              top=None if dlrm else top_cfg)
+            self.dlrm = None
+            if dlrm:
+                from paper_2403_00877_b200.dlrm import DLRM
+
+                self.dlrm = DLRM(self.model, 16, bottom=(512, 256), top=(512, 256), seed=0)
             gen = torch.Generator(device=dev).manual_seed(1234 + rank)
             if args.pool_dist == "powerlaw":
                 from paper_2403_00877_b200.sptt import powerlaw_lengths, random_kjt_lengths
@@ -406,9 +424,13 @@ def main():
                 self.batches = [{rank: random_kjt(F, B, args.rows, Lp, gen, dev)} for _ in range(4)]
             self.gout = {rank: (torch.randn(B, self.model.out_width, generator=gen, device=dev) * 1e-3).to(dtype)}
             self.labels = {rank: (torch.rand(B, generator=gen, device=dev) < 0.25).float()}  # synthetic CTR labels
+            # 13 Criteo-like dense features (padded to 16 columns, zero)
+            self.dense = {rank: torch.nn.functional.pad(torch.randn(B, 13, generator=gen, device=dev), (0, 3)).to(dtype)}
 
         def step(self, kj):
             m = self.model
+            if self.dlrm is not None:
+                return self.dlrm.train_step(kj, self.dense, self.labels)
             if m.top is not None:
                 return m.train_step_bce(kj, self.labels)
             return m.train_step(kj, self.gout)
@@ -457,8 +479,11 @@ def main():
             m = self.model
             self.st = {rank: KJT(self.batches[0][rank].lengths.clone(), self.batches[0][rank].values.clone(),
                                  self.batches[0][rank].nnz_per_feature, B)}
-            self.replay, self.outs = m.capture(self.st, self.gout, timers=timers,
-                                               labels=self.labels if m.top is not None else None)
+            if self.dlrm is not None:
+                self.replay, self.outs = self.dlrm.capture(self.st, self.dense, self.labels, timers=timers)
+            else:
+                self.replay, self.outs = m.capture(self.st, self.gout, timers=timers,
+                                                   labels=self.labels if m.top is not None else None)
             torch.cuda.synchronize()
 
         def timed_graph(self, K_, host_inputs=None):
@@ -507,7 +532,7 @@ def main():
                     if i + 1 < n:
                         prefetch(i + 1)
                     self.replay()
-                    if m.top is not None:  # the BCE loss of this step
+                    if m.top is not None or self.dlrm is not None:  # the BCE loss of this step
                         loss_buf[i:i + 1].copy_(outs[rank])
                     else:  # <y, g> of the synthetic upstream gradient
                         torch.dot(outs[rank].view(-1).float(), self.gout[rank].view(-1).float(), out=loss_buf[i])

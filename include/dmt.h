@@ -220,7 +220,12 @@ enum dmt_epilogue {
    * (dx0 = sum_l g_{l+1} * u_l read straight from the saved layer tensors, so
    * the per-layer DCN_BWD epilogues need no fp32 dx0 read-modify-write:
    * DCN_BWD with aux2 = NULL only writes g and gu). */
-  DMT_EPI_DCN_FINAL = 5
+  DMT_EPI_DCN_FINAL = 5,
+  /* MLP layers (the DLRM dense / over arch): d = max(acc + bias, 0) */
+  DMT_EPI_BIAS_RELU = 6,
+  /* MLP backward: d = acc * (x0 > 0) -- dX of layer l masked by the saved
+   * ReLU output of layer l-1 (x0, in_dtype, row stride ld_x) */
+  DMT_EPI_RELU_BWD = 7
 };
 
 #define DMT_GEMM_MAX_PAIRS 4
@@ -317,6 +322,22 @@ int dmt_bce_with_logits(const void* z, const float* y, int64_t n, int32_t dtype,
 
 int dmt_sgd_dense(void* w, const float* g, int64_t n, float lr, int32_t dtype,
                   dmt_stream_t stream);
+
+/* DLRM pairwise dot interaction around SPTT (the C3 model; PAPER.md:359-361,
+ * TorchRec InteractionArch): V = [dense (B, dim) | sparse (B, num_sparse*dim)];
+ * out (B, dim + P), P = (num_sparse+1) num_sparse / 2: out[:, :dim] = dense,
+ * out[:, dim + i(i-1)/2 + j] = <V_i, V_j> for i > j.  fp32 accumulation.
+ * The backward writes d_dense (B, dim) and d_sparse (B, num_sparse*dim).
+ * dtype: DMT_F32 or DMT_BF16 (all operands). */
+/* dz = dy * (y > 0) (ReLU backward where no GEMM epilogue can take it) */
+int dmt_relu_bwd(const void* dy, const void* y, void* dz, int64_t n, int32_t dtype, dmt_stream_t stream);
+int dmt_dot_interaction_fwd(const void* dense, int64_t ld_dense, const void* sparse, int64_t ld_sparse,
+                            int32_t num_sparse, int32_t dim, int64_t batch, void* out, int64_t ld_out,
+                            int32_t dtype, dmt_stream_t stream);
+int dmt_dot_interaction_bwd(const void* grad_out, int64_t ld_grad_out, const void* dense, int64_t ld_dense,
+                            const void* sparse, int64_t ld_sparse, int32_t num_sparse, int32_t dim,
+                            int64_t batch, void* d_dense, int64_t ld_d_dense, void* d_sparse,
+                            int64_t ld_d_sparse, int32_t dtype, dmt_stream_t stream);
 
 /* Tower gradient all-reduce fused with SGD over NVLink peer memory (replaces
  * the NCCL all-reduce of TM gradients over the tower comm, SURVEY §8e "bwd",

@@ -21,3 +21,4 @@ reference's own ``tm_weight_jvp`` fixtures, the rest is "parity unpinned"
 
 from .towersim_port import *  # noqa: F401,F403
 from .backward import *  # noqa: F401,F403
+from .dlrm import *  # noqa: F401,F403

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libdmt.so")
 DT_F32, DT_BF16, DT_F64, DT_F16 = 0, 1, 2, 3
 POOL_NONE, POOL_SUM, POOL_MEAN = 0, 1, 2
 EPI_NONE, EPI_BIAS, EPI_CROSS, EPI_ACC, EPI_DCN_BWD, EPI_DCN_FINAL = 0, 1, 2, 3, 4, 5
+EPI_BIAS_RELU, EPI_RELU_BWD = 6, 7
 GEMM_TRANS_A, GEMM_TRANS_B, GEMM_AUX2_ACCUM, GEMM_SCALE_ACC = 1, 2, 4, 8
 GEMM_NO_PREFETCH, GEMM_BN_SHIFT, GEMM_CLUSTER, GEMM_SINGLE_CTA = 16, 8, 32, 64  # tuning overrides
 GEMM_MAX_PAIRS = 4
@@ -101,6 +102,9 @@ _SIGS = {
     "dmt_sgd_dense": (C.c_int, [vp, vp, i64, f32, i32, vp]),
     "dmt_peer_sum_sgd": (C.c_int, [vp, C.POINTER(C.c_void_p), i32, i64, f32, i32, vp]),
     "dmt_convert": (C.c_int, [vp, i32, vp, i32, i64, vp]),
+    "dmt_relu_bwd": (C.c_int, [vp, vp, vp, i64, i32, vp]),
+    "dmt_dot_interaction_fwd": (C.c_int, [vp, i64, vp, i64, i32, i32, i64, vp, i64, i32, vp]),
+    "dmt_dot_interaction_bwd": (C.c_int, [vp, i64, vp, i64, vp, i64, i32, i32, i64, vp, i64, vp, i64, i32, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

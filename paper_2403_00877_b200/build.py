@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "177", "-I", os.path.join(ROOT, "include")]
 SOURCES = ["gemm_kk.cu", "gemm_km.cu", "gemm_mk.cu", "gemm_mm.cu", "kjt.cu", "lookup.cu", "assemble.cu",
-           "gemm_sm100.cu"]
+           "gemm_sm100.cu", "interact.cu"]
 
 
 def _deps(src: str) -> list[str]:

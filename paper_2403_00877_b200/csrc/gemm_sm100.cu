@@ -107,7 +107,9 @@ int dmt_gemm_ex(const dmt_gemm_args* args, const void* a_lo, const void* b_lo, d
   // TMA: 16-byte aligned base and row strides
   if (((uintptr_t)a->a & 15) || ((uintptr_t)a->b & 15) || (a->lda * es) % 16 || (a->ldb * es) % 16)
     return DMT_ERR_UNSUPPORTED;
-  if ((a->epilogue == DMT_EPI_BIAS || a->epilogue == DMT_EPI_CROSS) && !a->bias) return DMT_ERR_DOMAIN;
+  if ((a->epilogue == DMT_EPI_BIAS || a->epilogue == DMT_EPI_CROSS || a->epilogue == DMT_EPI_BIAS_RELU) && !a->bias)
+    return DMT_ERR_DOMAIN;
+  if (a->epilogue == DMT_EPI_RELU_BWD && !a->x0) return DMT_ERR_DOMAIN;
   if (a->epilogue == DMT_EPI_CROSS && (!a->x0 || !a->xl)) return DMT_ERR_DOMAIN;
   if (a->epilogue == DMT_EPI_DCN_BWD && (!a->x0 || !a->aux || (a->aux2 && !a->xl))) return DMT_ERR_DOMAIN;
   if (a->npairs < 0 || a->npairs > DMT_GEMM_MAX_PAIRS) return DMT_ERR_DOMAIN;
@@ -118,7 +120,7 @@ int dmt_gemm_ex(const dmt_gemm_args* args, const void* a_lo, const void* b_lo, d
   if (a->epilogue == DMT_EPI_DCN_FINAL && !a->aux2 && !a->npairs) return DMT_ERR_DOMAIN;
   if ((a->epilogue == DMT_EPI_DCN_BWD || a->epilogue == DMT_EPI_DCN_FINAL) && a->out_dtype != a->in_dtype)
     return DMT_ERR_UNSUPPORTED;
-  if (a->epilogue > DMT_EPI_DCN_FINAL || a->epilogue < 0) return DMT_ERR_DOMAIN;
+  if (a->epilogue > DMT_EPI_RELU_BWD || a->epilogue < 0) return DMT_ERR_DOMAIN;
   cudaStream_t s = (cudaStream_t)stream;
   switch (a->in_dtype) {
     case DMT_BF16: return gemm::dispatch_major(a, nullptr, nullptr, s);

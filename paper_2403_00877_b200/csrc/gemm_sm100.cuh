@@ -469,7 +469,8 @@ template <typename TIN, typename TO, bool FEAT>
 __device__ __forceinline__ void epi_load(const Params& p, int64_t row, int64_t col, EpiIn<TIN, TO>& in) {
   const int64_t xo = row * p.ld_x + col;
   const int e = p.epilogue;
-  if (e == DMT_EPI_CROSS || e == DMT_EPI_DCN_BWD) rawld(reinterpret_cast<const TIN*>(p.x0) + xo, in.x0);
+  if (e == DMT_EPI_CROSS || e == DMT_EPI_DCN_BWD || e == DMT_EPI_RELU_BWD)
+    rawld(reinterpret_cast<const TIN*>(p.x0) + xo, in.x0);
   if (e == DMT_EPI_CROSS || (e == DMT_EPI_DCN_BWD && p.aux2)) rawld(reinterpret_cast<const TIN*>(p.xl) + xo, in.u);
   if ((e == DMT_EPI_ACC || e == DMT_EPI_DCN_BWD || e == DMT_EPI_DCN_FINAL) && p.beta != 0.f)
     rawld(reinterpret_cast<const TO*>(p.c) + row * p.ld_d + col, in.c);
@@ -504,13 +505,23 @@ template <typename TIN, typename TO, bool FEAT>
 __device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t col, float* v,
                                            const EpiIn<TIN, TO>& in, float* gs) {
   const int e = p.epilogue;
-  if (e == DMT_EPI_BIAS || e == DMT_EPI_CROSS) {
+  if (e == DMT_EPI_BIAS || e == DMT_EPI_CROSS || e == DMT_EPI_BIAS_RELU) {
     float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + col));
     float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + col + 4));
     v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
     v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
   }
+  if (e == DMT_EPI_BIAS_RELU) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
   const int64_t xo = row * p.ld_x + col;
+  if (e == DMT_EPI_RELU_BWD) {
+    float a[8];
+    rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.x0, a);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = a[j] > 0.f ? v[j] : 0.f;
+  }
   if (e == DMT_EPI_CROSS) {
     float a[8], b[8];
     rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.x0, a);
@@ -949,7 +960,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
         if (!row_ok) continue;
         const bool full = ncols == 32;
-        if (p.epilogue == DMT_EPI_BIAS || p.epilogue == DMT_EPI_CROSS) {
+        if (p.epilogue == DMT_EPI_BIAS || p.epilogue == DMT_EPI_CROSS || p.epilogue == DMT_EPI_BIAS_RELU) {
           if (full) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
@@ -960,6 +971,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += (i < ncols) ? p.bias[col + i] : 0.f;
           }
+        }
+        if (p.epilogue == DMT_EPI_BIAS_RELU) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        } else if (p.epilogue == DMT_EPI_RELU_BWD) {
+          const TIN* mp = reinterpret_cast<const TIN*>(p.x0) + row * p.ld_x + col;
+          float t[32];
+          if (full && p.vec_x) load32v<TIN>(mp, t);
+          else load32s<TIN>(mp, t, ncols);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = t[i] > 0.f ? v[i] : 0.f;
         }
         if (p.epilogue == DMT_EPI_CROSS) {
           const TIN* x0p = reinterpret_cast<const TIN*>(p.x0) + row * p.ld_x + col;
@@ -1196,7 +1218,8 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   for (int j = 0; j < a->npairs; ++j)
     p.vec_x = p.vec_x && ((uintptr_t)a->pair_g[j] % 16 == 0) && ((uintptr_t)a->pair_u[j] % 16 == 0);
   p.vec_store = p.vec_store && ((uintptr_t)p.c % 16 == 0);
-  const bool needs_x = a->epilogue == DMT_EPI_CROSS || a->epilogue == DMT_EPI_DCN_BWD || a->epilogue == DMT_EPI_DCN_FINAL;
+  const bool needs_x = a->epilogue == DMT_EPI_CROSS || a->epilogue == DMT_EPI_DCN_BWD ||
+                       a->epilogue == DMT_EPI_DCN_FINAL || a->epilogue == DMT_EPI_RELU_BWD;
   p.coalesced = p.vec_store && (!needs_x || p.vec_x);
   // fused bias-gradient column sums: every 32-column chunk must take a
   // coalesced epilogue path (n % 32 == 0) with 16-byte partial-row stores

@@ -319,6 +319,18 @@ def _aligned_operand(x: torch.Tensor) -> torch.Tensor:
 
 
 def split_tf32(x: torch.Tensor):
+    """(hi, lo) tf32 split.  A 2-D operand keeps a 16-byte aligned row stride
+    (TMA): a padded row-major view is split over its whole padded rows."""
+    if x.dim() == 2 and not x.is_contiguous():
+        k = x.shape[1]
+        if x.stride(1) == 1 and x.stride(0) >= k:
+            kp = x.stride(0)
+        else:
+            kp = (k + 3) // 4 * 4
+        full = torch.zeros((x.shape[0], kp), dtype=x.dtype, device=x.device)
+        full[:, :k].copy_(x)
+        hi, lo = split_tf32(full)
+        return hi[:, :k], lo[:, :k]
     x = x.contiguous()
     hi = torch.empty_like(x)
     lo = torch.empty_like(x)
@@ -397,6 +409,8 @@ def bce_with_logits(z: torch.Tensor, y: torch.Tensor, scale: float, dz: Optional
                     loss: Optional[torch.Tensor] = None):
     """dz = scale (sigmoid(z) - y); loss[0] = scale * sum BCE(z, y) (fp32)."""
     n = z.numel()
+    if not z.is_contiguous() or not y.is_contiguous():
+        raise ShapeError("bce_with_logits needs contiguous logits and labels")
     if y.numel() != n:
         raise ShapeError(f"labels {tuple(y.shape)} do not match logits {tuple(z.shape)}")
     if dz is None:
@@ -470,4 +484,46 @@ def convert(x: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
     out = torch.empty(x.shape, dtype=dtype, device=x.device)
     L.check(L.lib().dmt_convert(x.data_ptr(), _dt(x), out.data_ptr(), _dt(out), x.numel(), L.stream_ptr()),
             "dmt_convert")
+    return out
+
+
+# ------------------------------------------------------- DLRM interaction ---
+def dot_interaction_fwd(dense: torch.Tensor, sparse: torch.Tensor, num_sparse: int,
+                        out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """out (B, D + P) = [dense | <V_i, V_j> (i > j)], V = [dense | sparse as
+    (B, num_sparse, D)] (dmt_dot_interaction_fwd; P = (F+1)F/2)."""
+    B, D = dense.shape
+    width = D + (num_sparse + 1) * num_sparse // 2
+    if sparse.shape[0] != B or sparse.shape[1] < num_sparse * D:
+        raise ShapeError(f"sparse {tuple(sparse.shape)} does not hold {num_sparse} x {D} per sample")
+    if dense.dtype != sparse.dtype:
+        raise DomainError("dense and sparse operands must share a dtype")
+    if out is None:
+        out = torch.empty((B, width), dtype=dense.dtype, device=dense.device)
+    L.check(L.lib().dmt_dot_interaction_fwd(dense.data_ptr(), dense.stride(0), sparse.data_ptr(), sparse.stride(0),
+                                            num_sparse, D, B, out.data_ptr(), out.stride(0), _dt(dense),
+                                            L.stream_ptr()), "dmt_dot_interaction_fwd")
+    return out
+
+
+def dot_interaction_bwd(grad_out: torch.Tensor, dense: torch.Tensor, sparse: torch.Tensor, num_sparse: int,
+                        d_dense: Optional[torch.Tensor] = None, d_sparse: Optional[torch.Tensor] = None):
+    B, D = dense.shape
+    if d_dense is None:
+        d_dense = torch.empty_like(dense)
+    if d_sparse is None:
+        d_sparse = torch.empty((B, num_sparse * D), dtype=dense.dtype, device=dense.device)
+    L.check(L.lib().dmt_dot_interaction_bwd(grad_out.data_ptr(), grad_out.stride(0), dense.data_ptr(), dense.stride(0),
+                                            sparse.data_ptr(), sparse.stride(0), num_sparse, D, B,
+                                            d_dense.data_ptr(), d_dense.stride(0), d_sparse.data_ptr(),
+                                            d_sparse.stride(0), _dt(dense), L.stream_ptr()), "dmt_dot_interaction_bwd")
+    return d_dense, d_sparse
+
+
+def relu_bwd(dy: torch.Tensor, y: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """dz = dy * (y > 0) (contiguous operands)."""
+    if out is None:
+        out = torch.empty_like(dy)
+    L.check(L.lib().dmt_relu_bwd(dy.data_ptr(), y.data_ptr(), out.data_ptr(), dy.numel(), _dt(dy), L.stream_ptr()),
+            "dmt_relu_bwd")
     return out

@@ -164,7 +164,8 @@ class SPTT:
         self.backward(gx, dense_hook=top_step)
         return losses
 
-    def capture(self, kjts: dict, grads: Optional[dict], warmup: int = 2, timers=None, labels: Optional[dict] = None):
+    def capture(self, kjts: dict, grads: Optional[dict], warmup: int = 2, timers=None, labels: Optional[dict] = None,
+                step=None):
         """Capture one full train step (forward a-f, backward, optimizer
         updates) as a CUDA graph over the given static input buffers.
 
@@ -177,8 +178,9 @@ class SPTT:
         self.engine.uniform_nnz = True
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        step = (lambda: self.train_step_bce(kjts, labels)) if labels is not None else (
-            lambda: self.train_step(kjts, grads))
+        if step is None:  # a full-model step (e.g. dlrm.DLRM.train_step) may be passed in
+            step = (lambda: self.train_step_bce(kjts, labels)) if labels is not None else (
+                lambda: self.train_step(kjts, grads))
         with torch.cuda.stream(s):
             for _ in range(warmup):
                 step()
