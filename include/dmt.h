@@ -280,6 +280,13 @@ typedef struct dmt_gemm_args {
    * (128-row tile, 32-row quarter): fp32 [dmt_gemm_colsum_rows(m), n]; finish
    * with dmt_column_sum_parts.  Needs n % 32 == 0 and 16-byte aligned rows. */
   float* colsum_part;
+  /* split-K (few output tiles, long K: the dW GEMMs of the DLRM tower module
+   * and MLPs): ksplit > 1 partitions K into ksplit ranges computed by
+   * separate CTAs into splitk_ws (fp32, ksplit * m * n), then summed in split
+   * order (deterministic) with the NONE / ACC epilogue applied.  0/1 = off. */
+  int32_t ksplit;
+  int32_t pad2_;
+  float* splitk_ws;
 } dmt_gemm_args;
 
 /* rows of the colsum_part buffer for an m-row GEMM */

@@ -66,7 +66,7 @@ class GemmArgs(C.Structure):
         ("rows_per_group", i64), ("ld_group", i64),
         ("beta", f32), ("alpha", f32), ("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("flags", i32),
         ("npairs", i32), ("pad_", i32), ("pair_g", vp * GEMM_MAX_PAIRS), ("pair_u", vp * GEMM_MAX_PAIRS),
-        ("colsum_part", vp),
+        ("colsum_part", vp), ("ksplit", i32), ("pad2_", i32), ("splitk_ws", vp),
     ]
 
 

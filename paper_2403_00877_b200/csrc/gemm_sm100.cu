@@ -81,6 +81,63 @@ __global__ void colsum_parts_kernel(const float* __restrict__ part, int64_t rows
 }  // namespace gemm
 }  // namespace dmt
 
+namespace dmt {
+namespace gemm {
+// d = epi(sum_s ws[s]) over the split-K partials, s ascending (the first copied)
+template <typename TO>
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int S, int64_t m, int64_t n, TO* __restrict__ d,
+                                     int64_t ld_d, const TO* __restrict__ c, float alpha, float beta, int scale_acc,
+                                     int acc) {
+  const int64_t total = m * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / n, col = i - r * n;
+    float v = ws[i];
+    for (int s = 1; s < S; ++s) v += ws[(int64_t)s * total + i];
+    if (scale_acc) v *= alpha;
+    if (acc && beta != 0.f) v += beta * to_f<TO>(c[r * ld_d + col]);
+    d[r * ld_d + col] = from_f<TO>(v);
+  }
+}
+}  // namespace gemm
+}  // namespace dmt
+
+static int gemm_splitk(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cudaStream_t s) {
+  using namespace dmt;
+  const size_t es = dtype_size(a->in_dtype);
+  const int64_t num_kb = ceil_div(a->k * (int64_t)es, 128);
+  const int64_t kbs = ceil_div(num_kb, (int64_t)a->ksplit);
+  dmt_gemm_args w = *a;  // the partial products: plain fp32 GEMMs into the workspace
+  w.d = a->splitk_ws;
+  w.c = nullptr;
+  w.ld_d = a->n;
+  w.out_dtype = DMT_F32;
+  w.epilogue = DMT_EPI_NONE;
+  w.flags = a->flags & (DMT_GEMM_TRANS_A | DMT_GEMM_TRANS_B | DMT_GEMM_BN_MASK | DMT_GEMM_NO_PREFETCH);
+  w.flags |= DMT_GEMM_SINGLE_CTA;
+  w.beta = 0.f;
+  w.ksplit = (int32_t)ceil_div(num_kb, kbs);
+  int rc = gemm::dispatch_major(&w, a_lo, b_lo, s);
+  if (rc != DMT_OK) return rc;
+  const int64_t total = a->m * a->n;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), DMT_NUM_SMS * 8));
+  const int scale = (a->flags & DMT_GEMM_SCALE_ACC) != 0, acc = a->epilogue == DMT_EPI_ACC;
+  const void* c = a->c ? a->c : a->d;
+  switch (a->out_dtype) {
+    case DMT_F32:
+      gemm::splitk_reduce_kernel<float><<<grid, 256, 0, s>>>(a->splitk_ws, w.ksplit, a->m, a->n, (float*)a->d, a->ld_d,
+                                                            (const float*)c, a->alpha, a->beta, scale, acc);
+      break;
+    case DMT_BF16:
+      gemm::splitk_reduce_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+          a->splitk_ws, w.ksplit, a->m, a->n, (__nv_bfloat16*)a->d, a->ld_d, (const __nv_bfloat16*)c, a->alpha,
+          a->beta, scale, acc);
+      break;
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
 extern "C" {
 
 int64_t dmt_gemm_colsum_rows(int64_t m) { return 4 * dmt::ceil_div(m, (int64_t)dmt::gemm::kBlockM); }
@@ -122,6 +179,13 @@ int dmt_gemm_ex(const dmt_gemm_args* args, const void* a_lo, const void* b_lo, d
     return DMT_ERR_UNSUPPORTED;
   if (a->epilogue > DMT_EPI_RELU_BWD || a->epilogue < 0) return DMT_ERR_DOMAIN;
   cudaStream_t s = (cudaStream_t)stream;
+  if (a->ksplit > 1) {
+    if (!a->splitk_ws || (a->epilogue != DMT_EPI_NONE && a->epilogue != DMT_EPI_ACC) ||
+        a->rows_per_group > 0 || a->colsum_part)
+      return DMT_ERR_DOMAIN;
+    if (a->in_dtype == DMT_F32 && (!a_lo || !b_lo)) return DMT_ERR_DOMAIN;
+    return gemm_splitk(a, a_lo, b_lo, s);
+  }
   switch (a->in_dtype) {
     case DMT_BF16: return gemm::dispatch_major(a, nullptr, nullptr, s);
     case DMT_F16: return gemm::dispatch_major(a, nullptr, nullptr, s);

@@ -305,6 +305,8 @@ struct Params {
   const void* pu[DMT_GEMM_MAX_PAIRS];
   float* colsum;  // DCN_BWD: per (128-row tile, 32-row quarter) column sums of the stored gu
   int kchunk;     // tf32: K blocks accumulated per TMEM chunk (see gemm_kernel)
+  int ksplit;     // split-K: units = tiles x ksplit; split s covers K blocks [s*kbs, (s+1)*kbs)
+  int kbs;        //   and writes its raw fp32 accumulator at output rows + s * m (workspace)
 };
 
 // Output row address.  The grouped layout (per-feature DLRM projection rows
@@ -503,7 +505,7 @@ __device__ __forceinline__ float stored(float x) {
 
 template <typename TIN, typename TO, bool FEAT>
 __device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t col, float* v,
-                                           const EpiIn<TIN, TO>& in, float* gs) {
+                                           const EpiIn<TIN, TO>& in, float* gs, int64_t soff) {
   const int e = p.epilogue;
   if (e == DMT_EPI_BIAS || e == DMT_EPI_CROSS || e == DMT_EPI_BIAS_RELU) {
     float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + col));
@@ -569,7 +571,7 @@ __device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t
       }
     }
   }
-  TO* drow = out_row<TO>(p, row);
+  TO* drow = out_row<TO>(p, row + soff);  // soff: split-K workspace rows
   store8<TO>(drow + col, v);
 }
 
@@ -643,12 +645,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tiles_m = ceil_div(p.m, kBlockM), tiles_n = ceil_div(p.n, BN);
   // work unit = CL vertically adjacent tiles sharing n0 (one per cluster CTA)
-  const int64_t num_units = ceil_div(tiles_m, CL) * tiles_n;
+  const int64_t num_units = ceil_div(tiles_m, CL) * tiles_n * p.ksplit;
   const int crank = CL > 1 ? (int)cluster_rank() : 0;
   const int64_t u_first = blockIdx.x / CL, u_step = gridDim.x / CL;
-  auto unit_m0 = [&](int64_t u) { return (int64_t)(((u / tiles_n) * CL + crank) * kBlockM); };
-  auto unit_n0 = [&](int64_t u) { return (int64_t)((u % tiles_n) * BN); };
-  const int num_kb = (int)ceil_div(p.k * (int64_t)sizeof(TIN), kAtomBytes);
+  // unit u = (tile u / ksplit, K split u % ksplit)
+  auto unit_m0 = [&](int64_t u) { return (int64_t)((((u / p.ksplit) / tiles_n) * CL + crank) * kBlockM); };
+  auto unit_n0 = [&](int64_t u) { return (int64_t)(((u / p.ksplit) % tiles_n) * BN); };
+  const int num_kb_all = (int)ceil_div(p.k * (int64_t)sizeof(TIN), kAtomBytes);
+  auto unit_kb0 = [&](int64_t u) { return (int)(u % p.ksplit) * p.kbs; };
+  auto unit_kb1 = [&](int64_t u) { return min(num_kb_all, (int)(u % p.ksplit + 1) * p.kbs); };
   constexpr int K_ELEMS = kAtomBytes / sizeof(TIN);
   using OA = Operand<TIN, AMN>;
   using OB = Operand<TIN, BMN>;
@@ -703,7 +708,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         if (p.prefetch & 8) l2_prefetch_2d(&emaps.d2, n0, m0);
       }
       if (lane == 0) {
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb_end = unit_kb1(u);
+        for (int kb = unit_kb0(u); kb < kb_end; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
@@ -750,9 +756,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         // round-to-nearest fp32 adds in chunk order (deterministic).
         uint32_t tmem_t = tmem_d;
         bool first = true;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb_beg = unit_kb0(u), kb_end = unit_kb1(u);
+        for (int kb = kb_beg; kb < kb_end; ++kb) {
           if constexpr (KIND == 1) {
-            if (kb > 0 && kb % p.kchunk == 0) {
+            if (kb > kb_beg && (kb - kb_beg) % p.kchunk == 0) {
               if (tmem_t != tmem_d) umma_commit(&sfull[(s_it - 1) & 1]);  // previous chunk complete
               mbar_wait(&sempty[s_it & 1], ((s_it >> 1) & 1) ^ 1);
               tc_fence_after();
@@ -807,10 +814,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       const uint32_t acc_phase = (it >> 1) & 1;
       const int64_t m0 = unit_m0(u);
       const int64_t n0 = unit_n0(u);
+      const int64_t soff = (u % p.ksplit) * p.m;  // split-K: partial s lands at rows + s * m
       float* stile = stile_all + (warp - 2) * kStileFloats;
       if constexpr (KIND == 1) {
         // fold chunks 1.. of this tile into its accumulator (chunk order)
-        const int nch = (num_kb + p.kchunk - 1) / p.kchunk;
+        const int nch = (unit_kb1(u) - unit_kb0(u) + p.kchunk - 1) / p.kchunk;
         const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
         for (int c = 1; c < nch; ++c, ++e_it) {
           mbar_wait(&sfull[e_it & 1], (e_it >> 1) & 1);
@@ -879,7 +887,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           if (FEAT && p.colsum) {
             // stored gu back into the consumed staging slots, zero for rows >= m
             float gq[8];
-            if (r < p.m) epi_finish<TIN, TO, FEAT>(p, r, col, a, cur, gq);
+            if (r < p.m) epi_finish<TIN, TO, FEAT>(p, r, col, a, cur, gq, soff);
             else {
 #pragma unroll
               for (int j = 0; j < 8; ++j) gq[j] = 0.f;
@@ -888,7 +896,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             for (int j = 0; j < 8; ++j) stile[rl * 33 + c8 + j] = gq[j];
             if ((k & 3) == 3) colsum_chunk(p, stile, m0, q, col - c8, lane);
           } else if (r < p.m) {
-            epi_finish<TIN, TO, FEAT>(p, r, col, a, cur, nullptr);
+            epi_finish<TIN, TO, FEAT>(p, r, col, a, cur, nullptr, soff);
           }
         }
         __syncwarp();
@@ -905,7 +913,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       const bool row_ok = row < p.m;
       TO* drow = nullptr;
       if (row_ok)
-        drow = out_row<TO>(p, row);
+        drow = out_row<TO>(p, row + soff);
 #pragma unroll 1
       for (int c = half * kColsPerWarp; c < (half + 1) * kColsPerWarp; c += 32) {
         float v[32];
@@ -941,14 +949,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             float gq[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) gq[j] = 0.f;
-            if (r0 < p.m) epi_finish<TIN, TO, FEAT>(p, r0, col + c8, a, in0, (FEAT && p.colsum) ? gq : nullptr);
+            if (r0 < p.m) epi_finish<TIN, TO, FEAT>(p, r0, col + c8, a, in0, (FEAT && p.colsum) ? gq : nullptr, soff);
             if (FEAT && p.colsum) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) { stile[rl0 * 33 + c8 + j] = gq[j]; gq[j] = 0.f; }
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j) a[j] = stile[rl1 * 33 + c8 + j];
-            if (r1 < p.m) epi_finish<TIN, TO, FEAT>(p, r1, col + c8, a, in1, (FEAT && p.colsum) ? gq : nullptr);
+            if (r1 < p.m) epi_finish<TIN, TO, FEAT>(p, r1, col + c8, a, in1, (FEAT && p.colsum) ? gq : nullptr, soff);
             if (FEAT && p.colsum) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) stile[rl1 * 33 + c8 + j] = gq[j];
@@ -1209,6 +1217,14 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   p.scale_acc = (a->flags & DMT_GEMM_SCALE_ACC) != 0;
   p.alpha = a->alpha;
   p.kchunk = tf32_kchunk();
+  {
+    const int num_kb = (int)ceil_div(a->k * (int64_t)sizeof(TIN), kAtomBytes);
+    p.ksplit = a->ksplit > 1 ? a->ksplit : 1;
+    p.kbs = (int)ceil_div(num_kb, p.ksplit);
+    if constexpr (CL > 1) {
+      if (p.ksplit > 1) return DMT_ERR_UNSUPPORTED;
+    }
+  }
   p.beta = a->beta; p.out_dtype = a->out_dtype; p.in_dtype = a->in_dtype; p.epilogue = a->epilogue;
   size_t eo = dtype_size(a->out_dtype);
   p.vec_store = ((uintptr_t)a->d % 16 == 0) && ((a->ld_d * eo) % 16 == 0) && ((a->ld_group * eo) % 16 == 0);
@@ -1257,7 +1273,7 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
     }
     attr_set = true;
   }
-  int64_t tiles = ceil_div(a->m, kBlockM) * ceil_div(a->n, BN);
+  int64_t tiles = ceil_div(a->m, kBlockM) * ceil_div(a->n, BN) * p.ksplit;
   const int fmt = (KIND == 1) ? 2 : (std::is_same<TIN, __half>::value ? 0 : 1);
   uint32_t idesc = make_idesc(fmt, kBlockM * CL, BN, AMN, BMN);  // pair: M = 256
   if constexpr (CL == 1) {

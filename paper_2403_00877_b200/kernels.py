@@ -399,10 +399,29 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[
         epilogue=epilogue, flags=flags, npairs=len(pairs), colsum_part=L.ptr(colsum_part))
     if len(pairs) > L.GEMM_MAX_PAIRS:
         raise DomainError(f"at most {L.GEMM_MAX_PAIRS} epilogue pairs")
+    # split-K for few output tiles over a long K (tower-module / MLP weight
+    # gradients: e.g. DLRM dW_feat is 64 x 128 over K = T*B*F rows) -- one tile
+    # per CTA would leave all but a handful of the 148 SMs idle
+    ks = splitk_factor(m, n, k, a.element_size()) if (epilogue in (L.EPI_NONE, L.EPI_ACC) and not rows_per_group
+                                                      and colsum_part is None and not pairs) else 1
+    if ks > 1:
+        args.ksplit = ks
+        ws = torch.empty(ks * m * n, dtype=torch.float32, device=out.device)
+        args.splitk_ws = ws.data_ptr()
     for j, (g, u) in enumerate(pairs):
         args.pair_g[j], args.pair_u[j] = g.data_ptr(), u.data_ptr()
     L.check(L.lib().dmt_gemm_ex(C.byref(args), L.ptr(a_lo), L.ptr(b_lo), L.stream_ptr()), "dmt_gemm")
     return out
+
+
+def splitk_factor(m: int, n: int, k: int, es: int) -> int:
+    """K splits for an (m, n, k) GEMM: enough units to cover the SMs when the
+    output has few 128 x 128 tiles, each split keeping >= 8 K blocks."""
+    tiles = -(-m // 128) * -(-n // 128)
+    kb = -(-(k * es) // 128)
+    if tiles >= 74 or kb < 16:
+        return 1
+    return max(1, min(148 // tiles, kb // 8, 64))
 
 
 def bce_with_logits(z: torch.Tensor, y: torch.Tensor, scale: float, dz: Optional[torch.Tensor] = None,

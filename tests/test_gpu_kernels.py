@@ -310,3 +310,34 @@ def test_peer_sum_sgd_matches_rank_order_sum(dt, nsrc, n):
     assert torch.equal(got, want)
     with pytest.raises(DomainError):
         K.peer_sum_sgd(got, [g.to(torch.bfloat16) for g in gs], 0.05)
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("m,n,k", [(64, 128, 212_992), (256, 512, 8192), (1, 256, 8192), (416, 512, 8192),
+                                   (128, 64, 30_000)])
+def test_gemm_splitk_weight_grads(dt, m, n, k):
+    """Split-K (few output tiles, long K: the DLRM tower-module dW_feat over
+    T*B*F rows, MLP dW over the batch): A^T B from MN-major operands vs
+    float64, deterministic (fixed split order), and the fused-SGD ACC form."""
+    from paper_2403_00877_b200 import _lib as L
+    from paper_2403_00877_b200 import kernels as K
+
+    assert K.splitk_factor(m, n, k, 2 if dt == torch.bfloat16 else 4) > 1
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    a = (torch.randn(k, m, device="cuda", generator=g) * 0.1).to(dt)  # stored (k, m): A = a^T
+    b = (torch.randn(k, n, device="cuda", generator=g) * 0.1).to(dt)
+    out = torch.empty(m, n, device="cuda", dtype=torch.float32)
+    K.gemm(a, b, out, trans_a=True, trans_b=True)
+    again = torch.empty_like(out)
+    K.gemm(a, b, again, trans_a=True, trans_b=True)
+    want = a.double().T @ b.double()
+    tol = 1e-5 if dt == torch.float32 else 1e-2
+    mag = a.double().abs().T @ b.double().abs()
+    torch.cuda.synchronize()
+    assert ((out.double() - want).abs() <= tol * mag).all()
+    assert torch.equal(out, again)
+    w = torch.ones(m, n, device="cuda", dtype=dt)
+    K.gemm(a, b, w, trans_a=True, trans_b=True, epilogue=L.EPI_ACC, beta=1.0, alpha=-1e-3)
+    ww = 1.0 - 1e-3 * want
+    ulp = 2.0 ** -8 if dt == torch.bfloat16 else 2.0 ** -23
+    assert ((w.double() - ww).abs() <= ulp + tol * 1e-3 * mag).all()
