@@ -180,10 +180,12 @@ class SpttEngine:
         self.uniform_nnz = False
         self._side = None
         self._prepared: dict = {}
-        self.p2p_d = self.p2p_f = self.p2p_tm = False
+        self.p2p_d = self.p2p_f = self.p2p_tm = self.p2p_c = False
         self.direct_peer_x = False
         if getattr(fabric, "p2p", False) and sptt:
             self._init_peer_links()
+        elif getattr(fabric, "p2p", False) and plan.G > 1:
+            self._init_peer_links_flat()
 
     # ------------------------------------------------------- NVLink peers ----
     def _init_peer_links(self) -> None:
@@ -234,6 +236,24 @@ class SpttEngine:
                                       out_ld=dld, bag_begin=seg.bag_begin, nbags=seg.nbags, pooling=seg.pooling,
                                       row_begin=seg.row_begin, row_filter=seg.row_filter, key_base=seg.key_base))
             self.seg_fwd_p2p = K.SegmentTable(segs, dev)
+
+    def _init_peer_links_flat(self) -> None:
+        """The flat baseline over the same NVLink peer-store transport as SPTT
+        (a fair comparison of the two exchange algorithms): the lookup stores
+        every destination rank's block straight into that rank's step-c
+        receive buffer, and c^-1 stores each gradient block straight into its
+        owner's gradient buffer; a barrier completes each."""
+        p, dev = self.plan, self.device
+        (r,) = self.local
+        b = self.buf[r]
+        self.p2p_c = True
+        self.peer = self.fabric.share({"recv_c": b["recv_c"], "grad_x": b["grad_x"]})
+        segs = []
+        for seg, (pp, k, off, w) in zip(self.seg_fwd[r].segments, p.lookup_out_offsets(r, False)):
+            segs.append(K.Segment(weights=seg.weights, out=self.peer[pp]["recv_c"], out_offset=p.c_recv_offset(r, k),
+                                  out_ld=w, bag_begin=seg.bag_begin, nbags=seg.nbags, pooling=seg.pooling,
+                                  row_begin=seg.row_begin, row_filter=seg.row_filter, key_base=seg.key_base))
+        self.seg_fwd_p2p = K.SegmentTable(segs, dev)
 
     def _f_peer_copies(self, r: int) -> K.CopyTable:
         """Step f: Y block j -> the class member in tower j (its recv_f slot)."""
@@ -394,7 +414,7 @@ class SpttEngine:
             if save and self._prepare_with_lookup:
                 self._launch_prepare(r, offsets, recv_val[r], nnz)
             with self._t("lookup_fwd"):
-                table = self.seg_fwd_p2p if self.p2p_d else self.seg_fwd[r]
+                table = self.seg_fwd_p2p if (self.p2p_d or self.p2p_c) else self.seg_fwd[r]
                 K.pooled_lookup_fwd(table, offsets, recv_val[r], err)
             self._owner[r] = (offsets, recv_val[r], nnz)
             if save and not self._prepare_with_lookup:
@@ -457,9 +477,17 @@ class SpttEngine:
         world = list(range(p.G))
         send = {r: self.buf[r]["send_x"] for r in self.local}
         recv = {r: self.buf[r]["recv_c"] for r in self.local}
-        with self._t("exchange_c"):
-            fab.alltoallv(world, "c", send, {r: p.c_send_splits(r) for r in world}, recv,
-                          {r: p.c_recv_splits(r) for r in world}, self.trace, self.es)
+        if self.p2p_c:  # the lookup already stored every block in its receiver
+            (r,) = self.local
+            if self.trace is not None:
+                for j, dst in enumerate(world):
+                    self.trace.record_elements("c", r, dst, p.c_send_splits(r)[j], self.es)
+            with self._t("exchange_c"):
+                fab.barrier_(world)
+        else:
+            with self._t("exchange_c"):
+                fab.alltoallv(world, "c", send, {r: p.c_send_splits(r) for r in world}, recv,
+                              {r: p.c_recv_splits(r) for r in world}, self.trace, self.es)
         out = {}
         for r in self.local:
             self.asm_c[r].run()
@@ -655,6 +683,26 @@ class SpttEngine:
         world = list(range(p.G))
         gsend = {}
         fw = p.flat_width()
+        if self.p2p_c:
+            # c^-1 over NVLink: each feature block of this rank's output
+            # gradient goes straight into its owner's gradient buffer (the
+            # owner's step-c send layout, source block r)
+            (r,) = self.local
+            copies = []
+            for fb in p.c_blocks():
+                for pc in fb.pieces:
+                    o = self.placement.shards[pc.sid].rank
+                    k = p.k_of(pc.sid)
+                    copies.append((grad_out[r], fb.dst_col + pc.c0, fw, self.peer[o]["grad_x"],
+                                   r * p.B * p.SW[o] + p.B * p.pre[o][k], pc.ld, p.B, pc.width))
+            with self._t("exchange_c_bwd"):
+                K.Copy2DTable(copies, dev).run()
+                fab.barrier_(world)
+            if dense_hook is None:
+                self._embedding_update(lr, optimizer, eps)
+            else:
+                self.overlap_with_embedding_update(dense_hook, lr, optimizer, eps)
+            return
         for r in self.local:
             gc = self.buf[r]["grad_x"] if p.G == 1 else self._persist(r, "g_c", self.buf[r]["recv_c"])
             copies = []

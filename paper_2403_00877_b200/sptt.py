@@ -69,6 +69,15 @@ class SPTT:
             n = ds.pop()
             self.global_tm = TowerModule(tm, len(feats), n, init_tm_weights(tm, len(feats), n, salt=0),
                                          dtype=dtype, device=self.device)
+        # the flat global TM's world all-reduce + SGD over NVLink peer memory
+        # when the exchange runs over peers too (same transport as SPTT's
+        # tower reduction; rank-order fp32 sum, bit-identical replicas)
+        self._peer_dense = None
+        if (self.global_tm is not None and getattr(fabric, "p2p", False) and len(fabric.local_ranks) == 1
+                and 1 < topo.world_size <= L.MAX_PEER_SRCS):
+            bufs = {k: torch.empty(v.shape, dtype=torch.float32, device=self.device)
+                    for k, v in self.global_tm.w.items() if v.numel()}
+            self._peer_dense = (bufs, fabric.share({"gtm_" + k: v for k, v in bufs.items()}))
         # dense head above the exchange (data parallel, replicated on every
         # rank): the full DCN + SPTT model's top crossnet + logit projection,
         # a TowerModule over one "feature" of the whole SPTT output width
@@ -117,10 +126,24 @@ class SPTT:
             for k, v in self.global_tm.grads.items():
                 acc[k] = v.clone() if k not in acc else acc[k].add_(v)
 
+        if self._peer_dense is not None:
+            bufs = self._peer_dense[0]
+            for k, v in acc.items():
+                if k in bufs:
+                    bufs[k].view(v.shape).copy_(v)
+
         def dense_step():  # world all-reduce of the global TM grads + SGD
-            self.fabric.all_reduce_(list(range(self.plan.G)), acc)
-            self.global_tm.grads = acc
-            self.global_tm.sgd_step(self.dense_lr)
+            world = list(range(self.plan.G))
+            if self._peer_dense is not None:
+                bufs, peers = self._peer_dense
+                self.fabric.barrier_(world)
+                for k in bufs:
+                    K.peer_sum_sgd(self.global_tm.w[k], [peers[m]["gtm_" + k] for m in world], self.dense_lr)
+                self.global_tm.grads = {}  # the summed gradient is never materialised
+            else:
+                self.fabric.all_reduce_(world, acc)
+                self.global_tm.grads = acc
+                self.global_tm.sgd_step(self.dense_lr)
             if dense_hook is not None:
                 dense_hook()
 

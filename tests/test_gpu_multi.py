@@ -50,7 +50,7 @@ def _build(hosts, rph, dev, tm_kind="dcn"):
     return topo, layout, placement, assignment, pooling, cfg, kjts, B
 
 
-def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1, tm_kind="dcn"):
+def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1, tm_kind="dcn", mode="sptt"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
 
@@ -69,13 +69,13 @@ def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1, tm_kind="dcn
         Fab = PeerFabric if kind == "peer" else NcclFabric
         fab = Fab(world, rank, layout.group_width(topo), dev)
         dist_model = SPTT(topo, layout, placement, assignment, pooling, B, fab, tm=cfg, dtype=torch.float32,
-                          device=dev, lr=0.005)
+                          device=dev, lr=0.005, mode=mode)
         # reference: every rank on this GPU through the loopback fabric
         topo2, layout2, placement2, _, _, _, kjts2, _ = _build(hosts, rph, dev, tm_kind)
         ref = SPTT(topo2, layout2, placement2, assignment, pooling, B, LoopbackFabric(world, dev), tm=cfg,
-                   dtype=torch.float32, device=dev, lr=0.005)
+                   dtype=torch.float32, device=dev, lr=0.005, mode=mode)
         gen = np.random.default_rng(5)
-        O = dist_model.plan.out_width()
+        O = dist_model.out_width
         grads = {r: torch.from_numpy(gen.normal(size=(B, O)).astype(np.float32)).to(dev) for r in range(world)}
         # lr is small: at W = 4 every tower module sees 4B rows and lr 0.05
         # drives the DCN (quadratic in x) into divergence by step 3 -- two
@@ -91,7 +91,9 @@ def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1, tm_kind="dcn
         # The peer fabric sums the members' TM gradients in tower-rank order
         # (dmt_peer_sum_sgd), exactly as the loopback engine does: outputs,
         # TM weights and embedding shards must then be bit-identical at any W.
-        W = layout.group_width(topo)
+        # the group whose dense gradients are all-reduced: the tower (SPTT) or
+        # the world (the flat baseline's global TM)
+        W = layout.group_width(topo) if mode == "sptt" else topo.world_size
         exact = kind == "peer"
         ok, worst = True, 0.0
         for step in range(steps):  # several steps: peer-written buffers are reused
@@ -117,6 +119,10 @@ def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1, tm_kind="dcn
             for k, w in dist_model.tms[t].w.items():
                 if not torch.equal(w, ref.tms[t].w[k]):
                     ok, worst = False, float((w.double() - ref.tms[t].w[k].double()).abs().max())
+        if exact and dist_model.global_tm is not None:
+            for k, w in dist_model.global_tm.w.items():
+                if not torch.equal(w, ref.global_tm.w[k]):
+                    ok, worst = False, float((w.double() - ref.global_tm.w[k].double()).abs().max())
         q.put((rank, bool(ok), None if ok else f"worst out error {worst:.3e}"))
     except Exception:  # pragma: no cover
         import traceback
@@ -139,6 +145,32 @@ def test_distributed_step_matches_loopback(hosts, rph, kind, steps, tm_kind):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, hosts, rph, q, kind, steps, tm_kind)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, err in res:
+        assert ok, f"rank {rank}: {err}"
+
+
+@pytest.mark.parametrize("kind", ["nccl", "peer"])
+@pytest.mark.parametrize("hosts,rph", [(2, 1), (2, 2), (4, 1)])
+def test_distributed_flat_baseline_matches_loopback(hosts, rph, kind):
+    """The flat all-to-all baseline (global DCN) over NCCL and over the NVLink
+    peer-store transport SPTT uses: the peer form (lookup -> receivers'
+    buffers, c^-1 -> owners', global TM peer all-reduce) must equal the
+    loopback engine bit for bit."""
+    world = hosts * rph
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, hosts, rph, q, kind, 3, "dcn", "flat"))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
