@@ -738,7 +738,7 @@ def main():
         result["flat_baseline"] = {"value": N * B * args.steps / (fr["total_ms"] / 1000.0),
                                    "ms_per_step": fr["ms_step"], "exposed_comm_ms_per_step": fr["ph"].get("exchange", 0.0),
                                    "phases_ms_per_step": fr["ph"], "exchange_bytes": fex, "exchange_parts": fparts,
-                                   "fabric": "nccl all-to-all"}
+                                   "fabric": "nvlink peer stores + barrier" if args.fabric == "peer" else "nccl all-to-all"}
         del flat
     else:
         del arm

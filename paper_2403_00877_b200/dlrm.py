@@ -152,6 +152,12 @@ class DLRM:
         sp = self.sptt
         p = sp.plan
         D = None
+        if p.feature_towers is None:  # the flat baseline: the raw embeddings interact
+            ds = {p.dims[f] for f in p.features}
+            if len(ds) != 1 or sp.global_tm is not None:
+                raise DomainError("flat DLRM needs one embedding dim and no global tower module")
+            D = ds.pop()
+            return D, sp.out_width // D
         for t in range(p.T):
             cfg = sp.tm_cfg[t]
             if cfg.kind == "dlrm":

@@ -227,3 +227,40 @@ class PeerFabric(NcclFabric):
         if len(group) == 1:
             return
         self.dist.all_reduce(self._flag, group=self._pg(group))
+
+
+def slice_bounds(n: int, parts: int, i: int, align: int = 16) -> tuple[int, int]:
+    """[begin, end) of part i when n elements are split into ``parts`` nearly
+    equal, ``align``-aligned pieces."""
+    step = -(-n // parts)
+    step = -(-step // align) * align
+    return min(n, i * step), min(n, (i + 1) * step)
+
+
+def peer_allreduce_sgd(fabric, group, weights: dict, peer_g: dict, peer_w: dict, lr: float, device) -> None:
+    """Data-parallel gradient all-reduce fused with SGD over NVLink peer memory
+    as a reduce-scatter + all-gather: member i sums slice i of every member's
+    fp32 gradient buffer (group order -- bit-identical to the loopback
+    engine's rank-order sum), applies SGD to that slice of its own replica,
+    then every member copies the other members' updated slices.  Per member
+    ~(N-1)/N x (4 + weight bytes) per parameter cross the links, against
+    (N-1) x 4 for every member reading every peer's whole gradient.
+    ``peer_g[m][k]`` / ``peer_w[m][k]``: member m's gradient buffer / weight."""
+    me = fabric.rank
+    pos = group.index(me)
+    n_grp = len(group)
+    fabric.barrier_(group)  # every member's gradient buffers are complete
+    for k, w in weights.items():
+        b, e = slice_bounds(w.numel(), n_grp, pos)
+        K.peer_sum_sgd(w, [peer_g[m][k] for m in group], lr, b, e)
+    fabric.barrier_(group)  # every member's slice is updated
+    copies = []
+    for k, w in weights.items():
+        es = w.element_size()
+        for i, m in enumerate(group):
+            if m == me:
+                continue
+            b, e = slice_bounds(w.numel(), n_grp, i)
+            if e > b:
+                copies.append((peer_w[m][k].data_ptr() + b * es, w.data_ptr() + b * es, (e - b) * es))
+    K.CopyTable(copies, device).run()

@@ -486,17 +486,23 @@ def sgd_dense(w: torch.Tensor, g: torch.Tensor, lr: float) -> None:
             "dmt_sgd_dense")
 
 
-def peer_sum_sgd(w: torch.Tensor, grads: list, lr: float) -> None:
-    """w -= lr * sum(grads) (fp32, summed in list order); ``grads`` are this
-    rank's and peer-mapped (PeerBuffer) gradient buffers of w's size."""
+def peer_sum_sgd(w: torch.Tensor, grads: list, lr: float, begin: int = 0, end: Optional[int] = None) -> None:
+    """w -= lr * sum(grads) (fp32, summed in list order) over elements [begin,
+    end) (``begin`` a multiple of 4); ``grads`` are this rank's and
+    peer-mapped (PeerBuffer) gradient buffers of w's size."""
     import ctypes as C
 
+    end = w.numel() if end is None else end
     for g in grads:
         if g.dtype != torch.float32 or g.numel() != w.numel():
             raise DomainError("peer gradients must be fp32 buffers of the weight's size")
-    arr = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
-    L.check(L.lib().dmt_peer_sum_sgd(w.data_ptr(), arr, len(grads), w.numel(), lr, _dt(w), L.stream_ptr()),
-            "dmt_peer_sum_sgd")
+    if begin % 4 or not 0 <= begin <= end <= w.numel():
+        raise DomainError("peer_sum_sgd range must start at a multiple of 4 inside the weight")
+    if end == begin:
+        return
+    arr = (C.c_void_p * len(grads))(*[g.data_ptr() + 4 * begin for g in grads])
+    L.check(L.lib().dmt_peer_sum_sgd(w.data_ptr() + begin * w.element_size(), arr, len(grads), end - begin, lr,
+                                     _dt(w), L.stream_ptr()), "dmt_peer_sum_sgd")
 
 
 def convert(x: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:

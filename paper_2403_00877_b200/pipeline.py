@@ -31,7 +31,7 @@ from . import _lib as L
 from . import kernels as K
 from .embedding import POOL_MEAN, ROW_WISE, ShardedEmbedding
 from .errors import DomainError
-from .fabric import Fabric
+from .fabric import Fabric, peer_allreduce_sgd
 from .plan import ExchangePlan
 from .simnet import CommTrace
 
@@ -215,6 +215,7 @@ class SpttEngine:
             self.tm_gbuf = {k: torch.empty(v.shape, dtype=torch.float32, device=dev)
                             for k, v in self.tm[t].w.items() if v.numel()}
             share.update({"tmg_" + k: v for k, v in self.tm_gbuf.items()})
+            share.update({"tmw_" + k: self.tm[t].w[k] for k in self.tm_gbuf})
         self.peer = self.fabric.share(share)
         if self.p2p_d:
             # without row-wise shards (no summed pieces) the lookup stores each
@@ -636,16 +637,18 @@ class SpttEngine:
             for t, grads in tower_grads.items():
                 group = p.layout.tower_ranks(t, p.topo)
                 if self.p2p_tm:
-                    # NVLink: after the barrier every member sums the members'
-                    # gradient buffers in tower-rank order into its own replica
-                    # (identical on all members).  A member overwrites its
-                    # buffer only after the next step's step-d barrier, which
-                    # every reader passes after this side stream is joined.
-                    fab.barrier_(group)
-                    for k, g in grads.items():
-                        if g.numel():
-                            K.peer_sum_sgd(self.tm[t].w[k], [self.peer[m]["tmg_" + k] for m in group],
-                                           tm_lr if tm_lr is not None else lr)
+                    # NVLink reduce-scatter + SGD + all-gather: member i sums
+                    # slice i of the members' gradient buffers in tower-rank
+                    # order into its replica, then copies the others' updated
+                    # slices (bit-identical replicas).  A member overwrites its
+                    # gradient buffer / weights only after the next step's
+                    # step-d barrier, which every reader passes after this
+                    # side stream is joined.
+                    ks = [k for k in grads if k in self.tm_gbuf]
+                    peer_allreduce_sgd(fab, group, {k: self.tm[t].w[k] for k in ks},
+                                       {m: {k: self.peer[m]["tmg_" + k] for k in ks} for m in group},
+                                       {m: {k: self.peer[m]["tmw_" + k] for k in ks} for m in group},
+                                       tm_lr if tm_lr is not None else lr, dev)
                     # the tower-summed gradient is never materialised on this
                     # path (each member folds the peers' buffers straight into
                     # its weights): leave no rank-local partial behind that a

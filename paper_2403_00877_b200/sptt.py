@@ -20,7 +20,7 @@ from . import _lib as L
 from . import kernels as K
 from .errors import DomainError
 from .embedding import EmbeddingTable, ShardedEmbedding, TablePlan, shard_tables
-from .fabric import Fabric, LoopbackFabric
+from .fabric import Fabric, LoopbackFabric, peer_allreduce_sgd
 from .pipeline import KJT, SpttEngine
 from .plan import ExchangePlan
 from .topology import ClusterTopology, TowerLayout
@@ -77,7 +77,9 @@ class SPTT:
                 and 1 < topo.world_size <= L.MAX_PEER_SRCS):
             bufs = {k: torch.empty(v.shape, dtype=torch.float32, device=self.device)
                     for k, v in self.global_tm.w.items() if v.numel()}
-            self._peer_dense = (bufs, fabric.share({"gtm_" + k: v for k, v in bufs.items()}))
+            shared = {"gtm_" + k: v for k, v in bufs.items()}
+            shared.update({"gtw_" + k: self.global_tm.w[k] for k in bufs})
+            self._peer_dense = (bufs, fabric.share(shared))
         # dense head above the exchange (data parallel, replicated on every
         # rank): the full DCN + SPTT model's top crossnet + logit projection,
         # a TowerModule over one "feature" of the whole SPTT output width
@@ -136,9 +138,10 @@ class SPTT:
             world = list(range(self.plan.G))
             if self._peer_dense is not None:
                 bufs, peers = self._peer_dense
-                self.fabric.barrier_(world)
-                for k in bufs:
-                    K.peer_sum_sgd(self.global_tm.w[k], [peers[m]["gtm_" + k] for m in world], self.dense_lr)
+                peer_allreduce_sgd(self.fabric, world, {k: self.global_tm.w[k] for k in bufs},
+                                   {m: {k: peers[m]["gtm_" + k] for k in bufs} for m in world},
+                                   {m: {k: peers[m]["gtw_" + k] for k in bufs} for m in world},
+                                   self.dense_lr, self.device)
                 self.global_tm.grads = {}  # the summed gradient is never materialised
             else:
                 self.fabric.all_reduce_(world, acc)

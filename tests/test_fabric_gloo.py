@@ -82,6 +82,14 @@ def _worker(rank, world, port, hosts, rph, q):
         want, _, _, _ = oracle.tower_forward(lengths, values, feats, pooling, tabs, shards, assignment,
                                              oracle.OTopo(hosts, rph))
         ok = np.array_equal(out, want[rank])
+        # the flat baseline's step c over the world, same lookup kernels' layout
+        world_g = list(range(world))
+        sc = {rank: lookup_send_buffer(plan, tabs, rank, lengths, values, False)}
+        rc = a2a(world_g, sc, {r: plan.c_send_splits(r) for r in world_g}, {r: plan.c_recv_splits(r) for r in world_g})
+        flat = assemble_np(plan.c_blocks(), rc[rank], B, plan.flat_width())
+        want_flat, _, _, _ = oracle.baseline_forward(lengths, values, feats, pooling, tabs, shards,
+                                                     oracle.OTopo(hosts, rph))
+        ok = ok and np.array_equal(flat.reshape(B, -1), want_flat[rank])
         # tower all-reduce: sum of rank ids over the tower's ranks
         g = {"w": torch.full((3,), float(rank))}
         fab.all_reduce_(plan.group_of(rank), g)
@@ -95,8 +103,10 @@ def _worker(rank, world, port, hosts, rph, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("hosts,rph", [(2, 1), (2, 2), (4, 1)])
+@pytest.mark.parametrize("hosts,rph", [(2, 1), (2, 2), (4, 1), (2, 4), (4, 2)])
 def test_sptt_protocol_over_gloo(hosts, rph):
+    """Process-per-rank SPTT (steps a-f) and flat (step c) protocol, including
+    the north-star 8-rank layouts 2 towers x 4 and 4 towers x 2."""
     world = hosts * rph
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
