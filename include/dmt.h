@@ -99,7 +99,9 @@ typedef struct dmt_lookup_segment {
   int32_t nbags;       /* bags in this segment */
   int32_t pooling;     /* dmt_pooling */
   int32_t row_filter;  /* 1 = row-wise shard: filter + rebase */
-  int32_t pad_;
+  int32_t table_rows;  /* row-wise shards: rows of the whole table (> 0: indices
+                        * outside [0, table_rows) flag DMT_EBIT_INDEX even though
+                        * every shard filters them); 0 = no global check */
 } dmt_lookup_segment;
 
 /* Forward.  All segments share dtype.  Accumulation is fp32 (f32/bf16/f16) or

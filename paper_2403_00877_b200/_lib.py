@@ -37,7 +37,7 @@ class LookupSegment(C.Structure):
     _fields_ = [
         ("weights", vp), ("out", vp), ("state", vp),
         ("ld", i64), ("out_ld", i64), ("bag_begin", i64), ("row_begin", i64), ("key_base", i64),
-        ("rows", i32), ("width", i32), ("nbags", i32), ("pooling", i32), ("row_filter", i32), ("pad_", i32),
+        ("rows", i32), ("width", i32), ("nbags", i32), ("pooling", i32), ("row_filter", i32), ("table_rows", i32),
     ]
 
 

@@ -135,9 +135,10 @@ pooled_fwd_kernel(const dmt_lookup_segment* __restrict__ segs, const int64_t* __
     for (int u = 0; u < UN; ++u) {
       use[u] = false;
       if (k0 + u < end) {
-        int64_t r = (int64_t)__ldg(indices + k0 + u) - row_begin;
+        const int64_t gi = (int64_t)__ldg(indices + k0 + u);
+        int64_t r = gi - row_begin;
         bool in = r >= 0 && r < rows;
-        if (!in && !filt) bad = 1;
+        if (!in && (!filt || (sg.table_rows > 0 && (gi < 0 || gi >= sg.table_rows)))) bad = 1;
         use[u] = in;
         const T* rp = W + (in ? r : 0) * ld;
 #pragma unroll
@@ -189,9 +190,10 @@ pooled_fwd_scalar_kernel(const dmt_lookup_segment* __restrict__ segs, const int6
   for (int c = lane; c < sg.width; c += 32) {
     A acc = A(0);
     for (int64_t k = beg; k < end; ++k) {
-      int64_t r = (int64_t)__ldg(indices + k) - sg.row_begin;
+      const int64_t gi = (int64_t)__ldg(indices + k);
+      int64_t r = gi - sg.row_begin;
       if (r < 0 || r >= sg.rows) {
-        if (!sg.row_filter) bad = 1;
+        if (!sg.row_filter || (sg.table_rows > 0 && (gi < 0 || gi >= sg.table_rows))) bad = 1;
         continue;
       }
       acc += (A)to_d<T>(W[r * sg.ld + c]);

@@ -120,6 +120,7 @@ class Segment:
     row_filter: bool = False
     key_base: int = 0
     state: Optional[torch.Tensor] = None
+    table_rows: int = 0  # row-wise shards: global index range check (0 = off)
 
     def struct(self) -> L.LookupSegment:
         w = self.weights
@@ -138,7 +139,7 @@ class Segment:
             nbags=self.nbags,
             pooling=self.pooling,
             row_filter=1 if self.row_filter else 0,
-            pad_=0,
+            table_rows=self.table_rows,
         )
 
 

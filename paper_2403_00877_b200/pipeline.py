@@ -235,7 +235,8 @@ class SpttEngine:
                     dst, doff, dld = self.peer[m]["recv_d"], p.d_recv_offset(m, r, k) + j * p.B * w, w
                 segs.append(K.Segment(weights=seg.weights, out=dst, out_offset=doff,
                                       out_ld=dld, bag_begin=seg.bag_begin, nbags=seg.nbags, pooling=seg.pooling,
-                                      row_begin=seg.row_begin, row_filter=seg.row_filter, key_base=seg.key_base))
+                                      row_begin=seg.row_begin, row_filter=seg.row_filter, key_base=seg.key_base,
+                                      table_rows=seg.table_rows))
             self.seg_fwd_p2p = K.SegmentTable(segs, dev)
 
     def _init_peer_links_flat(self) -> None:
@@ -253,7 +254,8 @@ class SpttEngine:
         for seg, (pp, k, off, w) in zip(self.seg_fwd[r].segments, p.lookup_out_offsets(r, False)):
             segs.append(K.Segment(weights=seg.weights, out=self.peer[pp]["recv_c"], out_offset=p.c_recv_offset(r, k),
                                   out_ld=w, bag_begin=seg.bag_begin, nbags=seg.nbags, pooling=seg.pooling,
-                                  row_begin=seg.row_begin, row_filter=seg.row_filter, key_base=seg.key_base))
+                                  row_begin=seg.row_begin, row_filter=seg.row_filter, key_base=seg.key_base,
+                                  table_rows=seg.table_rows))
         self.seg_fwd_p2p = K.SegmentTable(segs, dev)
 
     def _f_peer_copies(self, r: int) -> K.CopyTable:
@@ -338,7 +340,9 @@ class SpttEngine:
             segs.append(K.Segment(weights=self.weights[sid], out=out, out_offset=off, out_ld=w,
                                   bag_begin=(pp * p.S[r] + k) * p.B, nbags=p.B, pooling=code,
                                   row_begin=sh.row_range[0], row_filter=sh.scheme == ROW_WISE,
-                                  key_base=key_base[sid], state=self.state.get(sid)))
+                                  key_base=key_base[sid], state=self.state.get(sid),
+                                  table_rows=self.placement.tables[sh.table_id].rows if sh.scheme == ROW_WISE
+                                  else 0))
         return K.SegmentTable(segs, self.device)
 
     def _assemble_table(self, fblocks, src: torch.Tensor, dst: torch.Tensor, rows: int) -> K.AssembleTable:

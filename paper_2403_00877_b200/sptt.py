@@ -32,7 +32,8 @@ class SPTT:
                  feature_towers: dict, pooling: dict, local_batch: int, fabric: Fabric,
                  tm: Optional[object] = None, dtype: torch.dtype = torch.float32, device=None,
                  mode: str = "sptt", lr: float = 0.01, optimizer: str = "sgd", eps: float = 1e-8,
-                 trace=None, top: Optional[TMConfig] = None, dense_lr: Optional[float] = None):
+                 trace=None, top: Optional[TMConfig] = None, dense_lr: Optional[float] = None,
+                 check_indices: bool = False):
         """``lr`` drives the embedding (sparse) update; ``dense_lr`` (default:
         ``lr``) the tower modules, the flat baseline's global TM and the top
         head -- recommendation models train the two at very different rates."""
@@ -94,6 +95,9 @@ class SPTT:
             self._labels_loss = {}
         self.lr, self.eps = lr, eps
         self.dense_lr = lr if dense_lr is None else dense_lr
+        # debug: validate every index against its table (TableLookupError, the
+        # reference's embedding.py:74-77 check); costs a host sync per step
+        self.check_indices = check_indices
         self.opt = L.OPT_ROWWISE_ADAGRAD if optimizer == "adagrad" else L.OPT_SGD
         if self.opt == L.OPT_ROWWISE_ADAGRAD:
             self.engine.enable_adagrad()
@@ -105,7 +109,7 @@ class SPTT:
         return self.plan.out_width() if self.plan.feature_towers is not None else self.plan.flat_width()
 
     def forward(self, kjts: dict, save: bool = True) -> dict:
-        outs = self.engine.forward(kjts, save=save)
+        outs = self.engine.forward(kjts, save=save, check_indices=self.check_indices)
         if self.global_tm is None:
             return outs
         self._gsaved = {}

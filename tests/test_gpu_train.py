@@ -364,3 +364,33 @@ def test_full_model_bce_step_loopback_vs_oracle(hosts, rph, top_kind):
         got = model.engine.weights[sid].double().cpu().numpy()
         (r0, r1), (c0, c1) = sh.row_range, sh.col_range
         _assert_sgd_rows(got, before[f][r0:r1, c0:c1], want[r0:r1, c0:c1], what=f"shard {sid}")
+
+
+@pytest.mark.parametrize("scheme", ["table_wise", "row_wise"])
+def test_train_api_check_indices(scheme):
+    """SPTT(check_indices=True) raises TableLookupError for an index outside
+    its table -- also for row-wise tables, where every shard filters the index
+    (embedding.py:74-77); off by default (no host sync)."""
+    import paper_2403_00877_b200 as P
+    from paper_2403_00877_b200.fabric import LoopbackFabric
+    from paper_2403_00877_b200.pipeline import KJT
+    from paper_2403_00877_b200.sptt import SPTT, build_world
+
+    F, rows, N, B = 4, 30, 8, 3
+    topo, layout, placement, assignment = build_world(2, 2, 1, F, rows, N, seed=1, scheme=scheme,
+                                                      shards_per_table=2)
+    G = topo.world_size
+    pooling = {f: "sum" for f in range(F)}
+    kjts = {}
+    for r in range(G):
+        lens = np.full(F * B, 2, dtype=np.int32)
+        vals = np.random.default_rng(r).integers(0, rows, size=2 * F * B).astype(np.int32)
+        if r == 1:
+            vals[5] = rows + 7  # out of range for its table
+        kjts[r] = KJT(torch.from_numpy(lens).to(dev()), torch.from_numpy(vals).to(dev()), [2 * B] * F, B)
+    ok = SPTT(topo, layout, placement, assignment, pooling, B, LoopbackFabric(G, dev()), dtype=torch.float32)
+    ok.forward(kjts, save=False)  # unchecked: no error, no sync
+    chk = SPTT(topo, layout, placement, assignment, pooling, B, LoopbackFabric(G, dev()), dtype=torch.float32,
+               check_indices=True)
+    with pytest.raises(P.TableLookupError):
+        chk.forward(kjts, save=False)
