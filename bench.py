@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--pool", type=int, default=20)
     ap.add_argument("--pool-dist", default="fixed", choices=["fixed", "powerlaw"],
                     help="fixed L = --pool (C2/C3), or power-law lengths with mean --pool, max 200 (C5; ragged "
-                         "nnz -> eager steps, no CUDA graph)")
+                         "nnz through the capacity-padded step a, CUDA-graph replayed)")
     ap.add_argument("--batch", type=int, default=8192)
     ap.add_argument("--tm", default="dcn", choices=["dcn", "dlrm", "passthrough"])
     ap.add_argument("--tm-out", type=int, default=64)
@@ -420,6 +420,14 @@ def main():
 
                 self.batches = [{rank: random_kjt_lengths(powerlaw_lengths(F, B, 100 * i + rank, mean=float(Lp)),
                                                           args.rows, gen, dev)} for i in range(4)]
+                # capacity-padded step a: per-feature capacity = the largest
+                # nnz of any rank's batch (no count exchange, CUDA-graph capturable)
+                cap = torch.tensor([max(bt[rank].nnz_per_feature[f] for bt in self.batches) for f in range(F)],
+                                   dtype=torch.int64, device=dev)
+                if world > 1:
+                    dist.all_reduce(cap, op=dist.ReduceOp.MAX)
+                cap = [(int(c) + 63) // 64 * 64 for c in cap.cpu()]
+                self.model.set_capacity(cap)
             else:
                 self.batches = [{rank: random_kjt(F, B, args.rows, Lp, gen, dev)} for _ in range(4)]
             self.gout = {rank: (torch.randn(B, self.model.out_width, generator=gen, device=dev) * 1e-3).to(dtype)}
@@ -477,7 +485,13 @@ def main():
 
         def capture(self, timers=None):
             m = self.model
-            self.st = {rank: KJT(self.batches[0][rank].lengths.clone(), self.batches[0][rank].values.clone(),
+            v0 = self.batches[0][rank].values
+            if m.engine.capacity is not None:  # ragged: a static values buffer of the capacity
+                vals = torch.zeros(sum(m.engine.capacity), dtype=v0.dtype, device=dev)
+                vals[: v0.numel()].copy_(v0)
+            else:
+                vals = v0.clone()
+            self.st = {rank: KJT(self.batches[0][rank].lengths.clone(), vals,
                                  self.batches[0][rank].nnz_per_feature, B)}
             if self.dlrm is not None:
                 self.replay, self.outs = self.dlrm.capture(self.st, self.dense, self.labels, timers=timers)
@@ -498,7 +512,9 @@ def main():
                 # a device staging buffer on a copy stream while step i runs; each
                 # step's loss is read back to pinned host memory asynchronously.
                 cs = torch.cuda.Stream()
-                stage = [(torch.empty_like(st[rank].lengths), torch.empty_like(st[rank].values)) for _ in range(2)]
+                nv = max(h[1].numel() for h in host_inputs)
+                stage = [(torch.empty_like(st[rank].lengths), torch.empty(nv, dtype=st[rank].values.dtype, device=dev))
+                         for _ in range(2)]
                 ready = [torch.cuda.Event() for _ in range(2)]
                 free = [torch.cuda.Event() for _ in range(2)]
                 losses = torch.zeros(max(K_, 1), dtype=torch.float32).pin_memory()
@@ -509,7 +525,7 @@ def main():
                     with torch.cuda.stream(cs):
                         cs.wait_event(free[j % 2])
                         stage[j % 2][0].copy_(hl, non_blocking=True)
-                        stage[j % 2][1].copy_(hv, non_blocking=True)
+                        stage[j % 2][1][: hv.numel()].copy_(hv, non_blocking=True)
                         ready[j % 2].record(cs)
 
             def run(n):
@@ -517,7 +533,7 @@ def main():
                     for i in range(n):
                         src = self.batches[i % len(self.batches)][rank]
                         st[rank].lengths.copy_(src.lengths, non_blocking=True)
-                        st[rank].values.copy_(src.values, non_blocking=True)
+                        st[rank].values[: src.values.numel()].copy_(src.values, non_blocking=True)
                         self.replay()
                     return
                 for ev in free:
@@ -527,7 +543,8 @@ def main():
                     cur = i % 2
                     torch.cuda.current_stream().wait_event(ready[cur])
                     st[rank].lengths.copy_(stage[cur][0], non_blocking=True)
-                    st[rank].values.copy_(stage[cur][1], non_blocking=True)
+                    nvi = host_inputs[i % len(host_inputs)][1].numel()
+                    st[rank].values[:nvi].copy_(stage[cur][1][:nvi], non_blocking=True)
                     free[cur].record()
                     if i + 1 < n:
                         prefetch(i + 1)
@@ -561,8 +578,6 @@ def main():
             # the events are graph nodes: they must live as long as the graph
             gtimers = self.gtimers = PhaseTimers(external=True)
             try:
-                if args.pool_dist != "fixed":
-                    raise RuntimeError("ragged per-batch nnz: eager steps (step-a counts exchange per batch)")
                 self.capture(timers=gtimers)
                 total = self.timed_graph(K_)
                 ph = dict(gtimers.ms())  # phases of the last replay (events are graph nodes)
@@ -578,7 +593,7 @@ def main():
         def lookup_bytes(self):
             p = self.model.plan
             bags = p.owner_bags(rank)
-            nnz = self.model.engine._owner[rank][2]
+            nnz = int(self.model.engine._owner[rank][0][-1])  # actual occurrences (capacity mode pads)
             return nnz * Nd * self.es + nnz * 4 + (bags + 1) * 8 + bags * Nd * self.es, nnz, bags
 
         def unique_rows(self):

@@ -74,6 +74,16 @@ int dmt_kjt_bucketize(const int32_t* lengths, const int64_t* offsets, const int3
 
 /* Device-side slot offsets (when per-feature nnz is not known on the host):
  * slot_value_offset[s+1] - slot_value_offset[s] = nnz(slot_feature[s]). */
+/* Capacity-padded step a (ragged batches under CUDA graphs; no count
+ * exchange): slots are bucketized at fixed capacity offsets, the owner packs
+ * region seg (= src-major, shard order; bags seg*B .. seg*B+B-1) from
+ * src + seg_src_start[seg] to dst + offsets[seg*B], count from the packed
+ * offsets of the received lengths.  check_capacity sets *flag |= 1 when a
+ * feature's nnz exceeds its capacity (values past it would be dropped). */
+int dmt_kjt_compact(const int32_t* src, const int64_t* offsets, int32_t B, int32_t num_segments,
+                    const int64_t* seg_src_start, int32_t* dst, dmt_stream_t stream);
+int dmt_kjt_check_capacity(const int64_t* offsets, int32_t B, int32_t F, const int64_t* capacity, int32_t* flag,
+                           dmt_stream_t stream);
 int dmt_kjt_slot_offsets(const int64_t* offsets, int32_t B, int32_t num_slots,
                          const int32_t* slot_feature, int64_t* slot_value_offset,
                          dmt_stream_t stream);

@@ -81,6 +81,8 @@ _SIGS = {
     "dmt_lengths_to_offsets": (C.c_int, [vp, i64, vp, vp, vp]),
     "dmt_kjt_bucketize": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]),
     "dmt_kjt_slot_offsets": (C.c_int, [vp, i32, i32, vp, vp, vp]),
+    "dmt_kjt_compact": (C.c_int, [vp, vp, i32, i32, vp, vp, vp]),
+    "dmt_kjt_check_capacity": (C.c_int, [vp, i32, i32, vp, vp, vp]),
     "dmt_pooled_lookup_fwd": (C.c_int, [vp, vp, i32, vp, vp, i32, vp, vp]),
     "dmt_pooled_lookup_bwd_workspace_size": (sz, [i64, i64, i64]),
     "dmt_pooled_lookup_bwd": (C.c_int, [vp, vp, i32, vp, vp, i64, i64, i32, i32, f32, f32, vp, sz, vp]),

@@ -7,6 +7,7 @@
 // all-to-all that follows is NCCL (or an in-process copy) on these buffers.
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 
@@ -113,9 +114,14 @@ __global__ void bucketize_kernel(const int32_t* __restrict__ lengths, const int6
   const int64_t vend = offsets[(int64_t)(f + 1) * B];
   const int64_t nnz = vend - vbeg;
   const int64_t dst = slot_off[s];
+  // a slot whose values exceed its room (capacity-padded step a over its
+  // capacity; dmt_kjt_check_capacity flags it) ships empty bags instead:
+  // lengths and values stay consistent and no write leaves the slot
+  const bool over = nnz > slot_off[s + 1] - dst;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B; i += stride)
-    out_lengths[(int64_t)s * B + i] = lengths[(int64_t)f * B + i];
+    out_lengths[(int64_t)s * B + i] = over ? 0 : lengths[(int64_t)f * B + i];
+  if (over) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride)
     out_values[dst + i] = __ldg(values + vbeg + i);
 }
@@ -140,9 +146,52 @@ __global__ void slot_offsets_kernel(const int64_t* __restrict__ offsets, int32_t
   if (threadIdx.x == 0) out[num_slots] = carry;
 }
 
+// Capacity-padded step a (ragged batches under CUDA graphs): every slot of
+// the send buffer has a fixed capacity, so the step-a splits are static and
+// no count exchange / host sync is needed; the owner then packs each
+// (src, shard) region's actual values (count from the packed offsets of the
+// received lengths) back-to-back, which is the layout the lookup reads.
+__global__ void kjt_compact_kernel(const int32_t* __restrict__ src, const int64_t* __restrict__ offsets, int32_t B,
+                                   int32_t nseg, const int64_t* __restrict__ seg_src_start, int32_t* __restrict__ dst) {
+  for (int seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
+    const int64_t b0 = (int64_t)seg * B;
+    const int64_t beg = offsets[b0], cnt = offsets[b0 + B] - beg;
+    const int32_t* s = src + seg_src_start[seg];
+    int32_t* d = dst + beg;
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) d[i] = s[i];
+  }
+}
+
+// flag |= 1 if any feature's nnz exceeds its slot capacity
+__global__ void kjt_check_capacity_kernel(const int64_t* __restrict__ offsets, int32_t B, int32_t F,
+                                          const int64_t* __restrict__ cap, int32_t* __restrict__ flag) {
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x)
+    if (offsets[(int64_t)(f + 1) * B] - offsets[(int64_t)f * B] > cap[f]) atomicOr(flag, 1);
+}
+
 }  // namespace dmt
 
 extern "C" {
+
+int dmt_kjt_compact(const int32_t* src, const int64_t* offsets, int32_t B, int32_t num_segments,
+                    const int64_t* seg_src_start, int32_t* dst, dmt_stream_t stream) {
+  if (B < 0 || num_segments < 0) return DMT_ERR_DOMAIN;
+  if (num_segments == 0 || B == 0) return DMT_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>(num_segments, (int64_t)DMT_NUM_SMS * 8);
+  dmt::kjt_compact_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(src, offsets, B, num_segments, seg_src_start, dst);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_kjt_check_capacity(const int64_t* offsets, int32_t B, int32_t F, const int64_t* capacity, int32_t* flag,
+                           dmt_stream_t stream) {
+  if (B < 0 || F < 0) return DMT_ERR_DOMAIN;
+  if (F == 0) return DMT_OK;
+  dmt::kjt_check_capacity_kernel<<<(unsigned)dmt::ceil_div(F, 256), 256, 0, (cudaStream_t)stream>>>(offsets, B, F,
+                                                                                                   capacity, flag);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
 
 size_t dmt_lengths_to_offsets_workspace_size(int64_t n) {
   return sizeof(int64_t) * (size_t)(dmt::ceil_div(n, dmt::kScanTile) + 1);

@@ -860,6 +860,14 @@ inline int bucket_shift(int64_t nnz, int64_t key_space) {
 
 inline int64_t bucket_count(int64_t key_space, int bshift) { return (key_space >> bshift) + 1; }
 
+// keys of positions no bag covers (a capacity-padded step a hands the backward
+// more value slots than occurrences) must sort last and be skipped: fill with
+// the invalid key first
+__global__ void fill_u32_kernel(uint32_t* __restrict__ p, int64_t n, uint32_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
 __global__ void bwd_bucket_keys_kernel(const dmt_lookup_segment* __restrict__ segs,
                                        const int64_t* __restrict__ offsets, const int32_t* __restrict__ indices,
                                        uint32_t invalid, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
@@ -1305,6 +1313,11 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
   uint32_t* bcursor = (uint32_t*)(w + L.bcursor);
   uint64_t* items = (uint64_t*)(w + L.items);
   uint64_t* scratch = (uint64_t*)(w + L.scratch);
+  if (phase & 1) {
+    const unsigned fg = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nnz, 256), DMT_NUM_SMS * 8));
+    fill_u32_kernel<<<fg, 256, 0, s>>>(keys_in, nnz, invalid);
+    DMT_CHECK_LAUNCH();
+  }
   if ((phase & 1) && bucketed) {
     if (cudaMemsetAsync(bcounts, 0, (size_t)L.nbuckets * 4, s) != cudaSuccess) return DMT_ERR_CUDA;
     dim3 kg((unsigned)ceil_div((int64_t)max_b * 8, 256), n);

@@ -104,6 +104,17 @@ def kjt_bucketize(lengths, offsets, values, B: int, slot_feature: torch.Tensor,
             "dmt_kjt_bucketize")
 
 
+def kjt_compact(src: torch.Tensor, offsets: torch.Tensor, B: int, seg_src_start: torch.Tensor,
+                dst: torch.Tensor) -> None:
+    L.check(L.lib().dmt_kjt_compact(src.data_ptr(), offsets.data_ptr(), B, seg_src_start.numel(),
+                                    seg_src_start.data_ptr(), dst.data_ptr(), L.stream_ptr()), "dmt_kjt_compact")
+
+
+def kjt_check_capacity(offsets: torch.Tensor, B: int, capacity: torch.Tensor, flag: torch.Tensor) -> None:
+    L.check(L.lib().dmt_kjt_check_capacity(offsets.data_ptr(), B, capacity.numel(), capacity.data_ptr(),
+                                           flag.data_ptr(), L.stream_ptr()), "dmt_kjt_check_capacity")
+
+
 # --------------------------------------------------------- pooled lookup ----
 @dataclass
 class Segment:

@@ -23,7 +23,7 @@ from __future__ import annotations
 
 import os
 from dataclasses import dataclass
-from typing import Optional
+from typing import Optional, Sequence
 
 import torch
 
@@ -178,6 +178,7 @@ class SpttEngine:
         self._bwd_ws = {}
         self.timers: Optional[PhaseTimers] = None
         self.uniform_nnz = False
+        self.capacity: Optional[list] = None  # per-feature value capacity (set_capacity)
         self._side = None
         self._prepared: dict = {}
         self.p2p_d = self.p2p_f = self.p2p_tm = self.p2p_c = False
@@ -369,6 +370,40 @@ class SpttEngine:
             else:
                 self.seg_bwd[r] = self._segments(r, self.buf[r]["grad_x"], with_keys=True)
 
+    def set_capacity(self, capacity: Optional[Sequence[int]]) -> None:
+        """Capacity-padded step a for ragged batches (C5 power-law pooling)
+        without a host sync: every rank's send slot of feature f holds
+        ``capacity[f]`` values (>= that feature's nnz on any rank in any step),
+        so the step-a splits are static, the owner packs the received regions
+        on the device (dmt_kjt_compact) and the embedding backward sorts the
+        padded count with the unused slots keyed invalid.  A feature exceeding
+        its capacity sets a device flag (capacity_overflowed()).  None = off."""
+        p = self.plan
+        if capacity is None:
+            self.capacity = None
+            return
+        if len(capacity) != len(p.features):
+            raise DomainError("one capacity per feature position")
+        self.capacity = [int(c) for c in capacity]
+        dev = self.device
+        self._cap_dev = K.device_ints(self.capacity, torch.int64, dev)
+        self._cap_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._cap_seg = {}
+        for r in self.local:
+            caps = [self.capacity[p.fpos[p.shards[sid].table_id]] for sid in p.by_owner[r]]
+            C_r = sum(caps)
+            starts, acc = [], 0
+            for c in caps:
+                starts.append(acc)
+                acc += c
+            self._cap_seg[r] = K.device_ints([pp * C_r + s for pp in range(p.G) for s in starts] or [0],
+                                             torch.int64, dev)
+
+    def capacity_overflowed(self) -> bool:
+        """True if a capacity-padded step saw a feature over its capacity
+        (host sync; check it outside the timed loop)."""
+        return self.capacity is not None and bool(self._cap_flag.item())
+
     # ---------------------------------------------------------- forward ----
     def forward(self, kjts: dict, save: bool = False, check_indices: bool = False) -> dict:
         p, fab, dev = self.plan, self.fabric, self.device
@@ -380,7 +415,10 @@ class SpttEngine:
             if kj.B != p.B or kj.F != len(p.features):
                 raise DomainError("KJT shape does not match the plan")
             offs = kj.offsets if kj.offsets is not None else K.lengths_to_offsets(kj.lengths)
-            slot_offs = p.a_slot_value_offsets(kj.nnz_per_feature)
+            nnz_pf = kj.nnz_per_feature if self.capacity is None else self.capacity
+            if self.capacity is not None:
+                K.kjt_check_capacity(offs, p.B, self._cap_dev, self._cap_flag)
+            slot_offs = p.a_slot_value_offsets(nnz_pf)
             total = slot_offs[-1]
             send_len[r] = torch.empty(max(1, len(p.a_slots) * p.B), dtype=torch.int32, device=dev)
             send_val[r] = torch.empty(max(1, total), dtype=torch.int32, device=dev)
@@ -388,8 +426,8 @@ class SpttEngine:
                 so = K.device_ints(slot_offs, torch.int64, dev)
                 K.kjt_bucketize(kj.lengths, offs, kj.values, p.B, self.slot_feature, so, send_len[r], send_val[r])
             len_splits[r] = p.a_send_length_splits()
-            val_splits[r] = p.a_send_value_splits(kj.nnz_per_feature)
-        if self.uniform_nnz:
+            val_splits[r] = p.a_send_value_splits(nnz_pf)
+        if self.uniform_nnz or self.capacity is not None:
             # fixed pooling factors: every rank ships the same per-feature nnz,
             # so owner r receives val_splits[r][r] from every source and the
             # ragged step-a splits need no counts exchange (no host sync -> the
@@ -416,6 +454,11 @@ class SpttEngine:
         for r in self.local:
             offsets = K.lengths_to_offsets(recv_len[r][: p.owner_bags(r)])
             nnz = sum(recv_val_splits[r])
+            if self.capacity is not None:
+                # pack the capacity-padded (src, shard) regions back to back
+                packed = self._persist(r, "recv_val_packed", recv_val[r])
+                K.kjt_compact(recv_val[r], offsets, p.B, self._cap_seg[r][: p.G * p.S[r]], packed)
+                recv_val[r] = packed
             if save and self._prepare_with_lookup:
                 self._launch_prepare(r, offsets, recv_val[r], nnz)
             with self._t("lookup_fwd"):

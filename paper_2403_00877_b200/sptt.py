@@ -102,6 +102,11 @@ class SPTT:
         if self.opt == L.OPT_ROWWISE_ADAGRAD:
             self.engine.enable_adagrad()
 
+    def set_capacity(self, capacity) -> None:
+        """Ragged batches without a host sync (and under CUDA graphs): see
+        SpttEngine.set_capacity; ``capacity[f]`` >= feature f's nnz per rank."""
+        self.engine.set_capacity(capacity)
+
     @property
     def out_width(self) -> int:
         if self.global_tm is not None:
@@ -201,8 +206,9 @@ class SPTT:
 
         Returns (replay, outs): copy the next batch into ``kjts``' lengths /
         values in place, then call replay().  Requires fixed per-feature nnz
-        (uniform_nnz: no step-a counts exchange / host sync) and a fixed batch
-        shape.  Every launch inside is a libdmt kernel or an NCCL collective on
+        (uniform_nnz: no step-a counts exchange / host sync), or, for ragged
+        batches, per-feature capacities (set_capacity; the static values
+        buffer then holds sum(capacity) entries), and a fixed batch shape.  Every launch inside is a libdmt kernel or an NCCL collective on
         the capture stream; descriptor tables are content-cached, so replay
         issues no host work besides the graph launch."""
         self.engine.uniform_nnz = True

@@ -394,3 +394,84 @@ def test_train_api_check_indices(scheme):
                check_indices=True)
     with pytest.raises(P.TableLookupError):
         chk.forward(kjts, save=False)
+
+
+def _ragged_world(hosts, rph, seed=3):
+    from paper_2403_00877_b200.pipeline import KJT
+    from paper_2403_00877_b200.sptt import build_world, powerlaw_lengths
+
+    F, rows, N, B = 6, 80, 16, 32
+    topo, layout, placement, assignment = build_world(hosts, rph, 1, F, rows, N, seed=seed)
+    G = topo.world_size
+    batches = []
+    for i in range(4):
+        kj = {}
+        for r in range(G):
+            lens = powerlaw_lengths(F, B, 1000 * i + r, mean=6.0, cap=40)
+            vals = np.random.default_rng(7 * i + r).integers(0, rows, size=int(lens.sum())).astype(np.int32)
+            kj[r] = KJT(torch.from_numpy(lens.reshape(-1)).to(dev()), torch.from_numpy(vals).to(dev()),
+                        [int(x) for x in lens.sum(axis=1)], B)
+        batches.append(kj)
+    cap = [max(b[r].nnz_per_feature[f] for b in batches for r in range(G)) + 5 for f in range(F)]
+    return topo, layout, placement, assignment, batches, cap, F, B
+
+
+@pytest.mark.parametrize("hosts,rph", [(1, 1), (2, 2), (4, 1)])
+def test_capacity_padded_ragged_steps_match_exact_counts(hosts, rph):
+    """C5-style ragged batches: the capacity-padded step a (static splits, no
+    count exchange) gives the same outputs and table updates, bit for bit, as
+    the exact-count path; CUDA-graph replays of it equal eager steps bitwise."""
+    import paper_2403_00877_b200 as P
+    from paper_2403_00877_b200.fabric import LoopbackFabric
+    from paper_2403_00877_b200.pipeline import KJT
+    from paper_2403_00877_b200.sptt import SPTT
+
+    cfg = P.TMConfig(kind="dcn", out_dim=4, cross_layers=2, seed=1)
+
+    def model():
+        topo, layout, placement, assignment, batches, cap, F, B = _ragged_world(hosts, rph)
+        m = SPTT(topo, layout, placement, assignment, {f: "sum" for f in range(F)}, B,
+                 LoopbackFabric(topo.world_size, dev()), tm=cfg, dtype=torch.float32, lr=0.5, dense_lr=1e-3)
+        return m, batches, cap, B
+
+    exact, batches, cap, B = model()
+    padded, _, _, _ = model()
+    padded.set_capacity(cap)
+    G = len(batches[0])
+    g = {r: torch.full((B, exact.out_width), 0.01, device=dev()) for r in range(G)}
+    for bt in batches:
+        oe = exact.train_step(bt, g)
+        op = padded.train_step(bt, g)
+        for r in range(G):
+            assert torch.equal(oe[r], op[r])
+    assert not padded.engine.capacity_overflowed()
+    for sid, w in exact.engine.weights.items():
+        assert torch.equal(w, padded.engine.weights[sid])
+    # graph replay of the padded step == eager padded steps
+    graph, _, _, _ = model()
+    graph.set_capacity(cap)
+    eager, _, _, _ = model()
+    eager.set_capacity(cap)
+    st = {r: KJT(batches[0][r].lengths.clone(), torch.zeros(sum(cap), dtype=torch.int32, device=dev()),
+                 batches[0][r].nnz_per_feature, B) for r in range(G)}
+    for r in range(G):
+        st[r].values[: batches[0][r].values.numel()].copy_(batches[0][r].values)
+    replay, outs = graph.capture(st, g, warmup=2)
+    for _ in range(2):
+        eager.train_step(batches[0], g)
+    for i in (1, 2, 3):
+        for r in range(G):
+            st[r].lengths.copy_(batches[i][r].lengths)
+            st[r].values[: batches[i][r].values.numel()].copy_(batches[i][r].values)
+        replay()
+        oe = eager.train_step(batches[i], g)
+        torch.cuda.synchronize()
+        for r in range(G):
+            assert torch.equal(outs[r], oe[r]), (i, r)
+    for sid, w in eager.engine.weights.items():
+        assert torch.equal(w, graph.engine.weights[sid])
+    # a feature over its capacity raises the device flag
+    small, _, _, _ = model()
+    small.set_capacity([1] * len(cap))
+    small.forward(batches[0], save=False)
+    assert small.engine.capacity_overflowed()
