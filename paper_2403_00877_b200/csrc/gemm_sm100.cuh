@@ -1250,6 +1250,23 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   // it hides (+3..15 %), so those are left to the register-pipelined loads.
   (void)plain_rows;
   if (p.vec_x && a->epilogue == DMT_EPI_CROSS && BN <= 192) p.prefetch |= 1 | 2;
+  {
+    // experiment override: DMT_EPI_PREFETCH = bit mask (1 x0, 2 xl/u, 4 C, 8 dx0)
+    static const int forced = [] {
+      const char* e = getenv("DMT_EPI_PREFETCH");
+      return e ? atoi(e) : -1;
+    }();
+    if (forced >= 0 && p.vec_x) {
+      int m = 0;
+      if (needs_x || a->epilogue == DMT_EPI_RELU_BWD) m |= forced & 1;
+      if (a->epilogue == DMT_EPI_CROSS || (a->epilogue == DMT_EPI_DCN_BWD && a->aux2)) m |= forced & 2;
+      if ((a->epilogue == DMT_EPI_ACC || a->epilogue == DMT_EPI_DCN_BWD || a->epilogue == DMT_EPI_DCN_FINAL) &&
+          a->beta != 0.f)
+        m |= forced & 4;
+      if (a->aux2 && (a->epilogue == DMT_EPI_DCN_FINAL || (a->flags & DMT_GEMM_AUX2_ACCUM))) m |= forced & 8;
+      p.prefetch = m;
+    }
+  }
   if (a->flags & DMT_GEMM_NO_PREFETCH) p.prefetch = 0;
   EpiMaps em;
   memset(&em, 0, sizeof(em));

@@ -104,6 +104,13 @@ def kjt_bucketize(lengths, offsets, values, B: int, slot_feature: torch.Tensor,
             "dmt_kjt_bucketize")
 
 
+def kjt_slot_offsets(offsets: torch.Tensor, B: int, slot_feature: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """Device-side packed slot offsets: out[s+1] - out[s] = nnz of slot s."""
+    L.check(L.lib().dmt_kjt_slot_offsets(offsets.data_ptr(), B, slot_feature.numel(), slot_feature.data_ptr(),
+                                         out.data_ptr(), L.stream_ptr()), "dmt_kjt_slot_offsets")
+    return out
+
+
 def kjt_compact(src: torch.Tensor, offsets: torch.Tensor, B: int, seg_src_start: torch.Tensor,
                 dst: torch.Tensor) -> None:
     L.check(L.lib().dmt_kjt_compact(src.data_ptr(), offsets.data_ptr(), B, seg_src_start.numel(),

@@ -389,6 +389,13 @@ class SpttEngine:
         self._cap_dev = K.device_ints(self.capacity, torch.int64, dev)
         self._cap_flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self._cap_seg = {}
+        # device byte counters of step a: owner o's slots are a_slots[b_o:e_o]
+        bounds, s0 = [], 0
+        for o in range(p.G):
+            bounds.append((s0, s0 + len(p.by_owner[o])))
+            s0 += len(p.by_owner[o])
+        self._owner_slot_begin = torch.tensor([b for b, _ in bounds], dtype=torch.long, device=dev)
+        self._owner_slot_end = torch.tensor([e for _, e in bounds], dtype=torch.long, device=dev)
         for r in self.local:
             caps = [self.capacity[p.fpos[p.shards[sid].table_id]] for sid in p.by_owner[r]]
             C_r = sum(caps)
@@ -425,6 +432,15 @@ class SpttEngine:
             if p.a_slots:
                 so = K.device_ints(slot_offs, torch.int64, dev)
                 K.kjt_bucketize(kj.lengths, offs, kj.values, p.B, self.slot_feature, so, send_len[r], send_val[r])
+                if self.capacity is not None and self.trace is not None:
+                    # the payload is each slot's actual nnz: device counters
+                    packed = self.buf[r].get("a_slot_packed")
+                    if packed is None:
+                        packed = self.buf[r]["a_slot_packed"] = torch.empty(len(p.a_slots) + 1, dtype=torch.int64,
+                                                                            device=dev)
+                    K.kjt_slot_offsets(offs, p.B, self.slot_feature, packed)
+                    counts = packed[self._owner_slot_end] - packed[self._owner_slot_begin]
+                    self.trace.record_device("a", r, world, counts, 4)
             len_splits[r] = p.a_send_length_splits()
             val_splits[r] = p.a_send_value_splits(nnz_pf)
         if self.uniform_nnz or self.capacity is not None:
@@ -447,7 +463,8 @@ class SpttEngine:
             fab.alltoallv(world, "a_len", send_len, len_splits, recv_len,
                           {r: [p.S[r] * p.B] * p.G for r in self.local})
         with self._t("exchange_a"):
-            fab.alltoallv(world, "a", send_val, val_splits, recv_val, recv_val_splits, self.trace, 4)
+            fab.alltoallv(world, "a", send_val, val_splits, recv_val, recv_val_splits,
+                          None if self.capacity is not None else self.trace, 4)
         # step b: lookup (+ fused permute) on every owner
         self._owner = {}
         err = torch.zeros(1, dtype=torch.int32, device=dev) if check_indices else None

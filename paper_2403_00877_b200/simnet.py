@@ -26,15 +26,37 @@ class TraceEntry(NamedTuple):
 
 
 class CommTrace:
-    """simnet.py:55-107: append-only message log of one run."""
+    """simnet.py:55-107: append-only message log of one run.
+
+    Messages whose sizes only the device knows (the capacity-padded step a of
+    ragged batches: the payload is each slot's actual nnz, not its capacity)
+    are recorded from device counters (``record_device``) and resolved on the
+    first query -- one host read, outside the step."""
 
     def __init__(self, topo: ClusterTopology):
         self.topo = topo
-        self.entries: list[TraceEntry] = []
+        self._entries: list[TraceEntry] = []
+        self._pending: list = []
         self.wire_bytes: dict[str, int] = {}
 
+    @property
+    def entries(self) -> list[TraceEntry]:
+        self._flush()
+        return self._entries
+
     def record(self, label: str, src: int, dst: int, nbytes: int) -> None:
-        self.entries.append(TraceEntry(label, src, dst, nbytes, link_class(src, dst, self.topo)))
+        self._entries.append(TraceEntry(label, src, dst, nbytes, link_class(src, dst, self.topo)))
+
+    def record_device(self, label: str, src: int, dsts, counts, elem_bytes: int) -> None:
+        """counts: device int64 tensor of elements src sends to each of dsts
+        (e.g. from dmt_kjt_slot_offsets), read when the trace is queried."""
+        self._pending.append((label, src, list(dsts), counts.clone(), int(elem_bytes)))
+
+    def _flush(self) -> None:
+        while self._pending:
+            label, src, dsts, counts, eb = self._pending.pop(0)
+            for dst, n in zip(dsts, counts.cpu().tolist()):
+                self.record_elements(label, src, dst, int(n), eb)
 
     def record_elements(self, label: str, src: int, dst: int, elements: int, elem_bytes: int) -> None:
         self.record(label, src, dst, BYTES_PER_ELEMENT * int(elements))
@@ -76,5 +98,5 @@ class CommTrace:
         with open(path, encoding="utf-8") as fh:
             for line in fh:
                 label, src, dst, nbytes, link = line.rstrip("\n").split("\t")
-                trace.entries.append(TraceEntry(label, int(src), int(dst), int(nbytes), link))
+                trace._entries.append(TraceEntry(label, int(src), int(dst), int(nbytes), link))
         return trace

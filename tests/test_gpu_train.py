@@ -475,3 +475,27 @@ def test_capacity_padded_ragged_steps_match_exact_counts(hosts, rph):
     small.set_capacity([1] * len(cap))
     small.forward(batches[0], save=False)
     assert small.engine.capacity_overflowed()
+
+
+def test_capacity_padded_step_a_device_byte_counters():
+    """With a capacity-padded step a the host only knows capacities; the
+    CommTrace step-a bytes come from device counters (dmt_kjt_slot_offsets)
+    and equal the exact-count path's trace (the reference's payload_nbytes)."""
+    import paper_2403_00877_b200 as P
+    from paper_2403_00877_b200.fabric import LoopbackFabric
+    from paper_2403_00877_b200.sptt import SPTT
+
+    topo, layout, placement, assignment, batches, cap, F, B = _ragged_world(2, 2)
+    G = topo.world_size
+    traces = []
+    for padded in (False, True):
+        tr = P.CommTrace(topo)
+        m = SPTT(topo, layout, placement, assignment, {f: "sum" for f in range(F)}, B, LoopbackFabric(G, dev()),
+                 dtype=torch.float32, trace=tr)
+        if padded:
+            m.set_capacity(cap)
+        m.forward(batches[1], save=False)
+        traces.append(tr)
+    for label in ("a", "d", "f"):
+        assert traces[0].byte_totals(label) == traces[1].byte_totals(label), label
+    assert traces[0].sent_by_rank("a") == traces[1].sent_by_rank("a")
