@@ -74,6 +74,18 @@ int dmt_kjt_bucketize(const int32_t* lengths, const int64_t* offsets, const int3
 
 /* Device-side slot offsets (when per-feature nnz is not known on the host):
  * slot_value_offset[s+1] - slot_value_offset[s] = nnz(slot_feature[s]). */
+/* Step a over NVLink peer stores: slot s's lengths / values are written to
+ * slot_dst[s] = {int32* len, int32* val, int64 room} (device array; peer-mapped
+ * pointers for remote owners), values bounded by room (else empty bags). */
+typedef struct dmt_slot_dst {
+  int32_t* len;
+  int32_t* val;
+  int64_t room;
+} dmt_slot_dst;
+int dmt_kjt_bucketize_peer(const int32_t* lengths, const int64_t* offsets, const int32_t* values, int32_t B,
+                           int32_t num_slots, const int32_t* slot_feature, const void* slot_dst,
+                           dmt_stream_t stream);
+
 /* Capacity-padded step a (ragged batches under CUDA graphs; no count
  * exchange): slots are bucketized at fixed capacity offsets, the owner packs
  * region seg (= src-major, shard order; bags seg*B .. seg*B+B-1) from
@@ -366,6 +378,13 @@ int dmt_dot_interaction_bwd(const void* grad_out, int64_t ld_grad_out, const voi
  * DMT_MAX_PEER_SRCS; every member passing the same order gets bit-identical
  * replicas.  The caller orders it after a barrier on the peers' writes. */
 #define DMT_MAX_PEER_SRCS 8
+/* Completion barrier of a peer group over NVLink (see peer_barrier_kernel):
+ * epoch = this rank's device counter for the group kind; remote_slots[i] =
+ * other member i's (peer-mapped) flag for this rank, local_slots[i] = this
+ * rank's flag for member i (HOST arrays of n <= DMT_MAX_PEER_SRCS device
+ * pointers).  *err |= 1 if a member does not arrive within ~2^26 polls. */
+int dmt_peer_barrier(int32_t* epoch, int32_t* const* remote_slots, int32_t* const* local_slots, int32_t n,
+                     int32_t* err, dmt_stream_t stream);
 int dmt_peer_sum_sgd(void* w, const float* const* g, int32_t nsrc, int64_t n, float lr, int32_t dtype,
                      dmt_stream_t stream);
 

@@ -41,6 +41,10 @@ class LookupSegment(C.Structure):
     ]
 
 
+class SlotDst(C.Structure):
+    _fields_ = [("len", vp), ("val", vp), ("room", i64)]
+
+
 class AssembleBlock(C.Structure):
     _fields_ = [("dst_col", i64), ("width", i32), ("nsrc", i32), ("first_src", i32), ("groups", C.c_uint32)]
 
@@ -82,6 +86,7 @@ _SIGS = {
     "dmt_kjt_bucketize": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]),
     "dmt_kjt_slot_offsets": (C.c_int, [vp, i32, i32, vp, vp, vp]),
     "dmt_kjt_compact": (C.c_int, [vp, vp, i32, i32, vp, vp, vp]),
+    "dmt_kjt_bucketize_peer": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp]),
     "dmt_kjt_check_capacity": (C.c_int, [vp, i32, i32, vp, vp, vp]),
     "dmt_pooled_lookup_fwd": (C.c_int, [vp, vp, i32, vp, vp, i32, vp, vp]),
     "dmt_pooled_lookup_bwd_workspace_size": (sz, [i64, i64, i64]),
@@ -103,6 +108,7 @@ _SIGS = {
     "dmt_cross_bwd_pointwise": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, vp]),
     "dmt_sgd_dense": (C.c_int, [vp, vp, i64, f32, i32, vp]),
     "dmt_peer_sum_sgd": (C.c_int, [vp, C.POINTER(C.c_void_p), i32, i64, f32, i32, vp]),
+    "dmt_peer_barrier": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), i32, vp, vp]),
     "dmt_convert": (C.c_int, [vp, i32, vp, i32, i64, vp]),
     "dmt_relu_bwd": (C.c_int, [vp, vp, vp, i64, i32, vp]),
     "dmt_dot_interaction_fwd": (C.c_int, [vp, i64, vp, i64, i32, i32, i64, vp, i64, i32, vp]),

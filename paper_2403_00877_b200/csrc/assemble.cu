@@ -255,6 +255,43 @@ struct PeerSrcs {
   const float* g[DMT_MAX_PEER_SRCS];
 };
 
+// Device barrier over NVLink peer memory (replaces the 1-float NCCL
+// all-reduce the peer fabric used as a completion barrier): each member bumps
+// its epoch for this group kind, release-stores it into every other member's
+// flag slot for it (system scope, over NVLink), then acquire-spins until every
+// other member's epoch arrived in its own slots.  The preceding kernels in
+// stream order happen-before the release; the acquire orders the following
+// kernels' reads of the peers' stores after it.  Epochs live on the device, so
+// the same launch replays correctly from a CUDA graph.
+struct BarrierSlots {
+  int32_t* remote[DMT_MAX_PEER_SRCS];  // member i's flag slot for this rank (peer-mapped)
+  int32_t* local[DMT_MAX_PEER_SRCS];   // this rank's flag slot for member i
+};
+
+__global__ void peer_barrier_kernel(int32_t* epoch, const __grid_constant__ BarrierSlots s, int n, int32_t* err) {
+  __shared__ int32_t e;
+  if (threadIdx.x == 0) {
+    e = *epoch + 1;
+    *epoch = e;
+  }
+  __syncthreads();
+  const int i = threadIdx.x;
+  if (i < n) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(s.remote[i]), "r"(e) : "memory");
+    int32_t v = 0;
+    long long spins = 0;
+    do {
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(s.local[i]) : "memory");
+      if (++spins > (1ll << 26)) {  // a peer never arrived: flag it instead of hanging the GPU
+        if (err) atomicOr(err, 1);
+        break;
+      }
+    } while (v < e);
+  }
+  __syncthreads();
+}
+
 template <typename T>
 __global__ void peer_sum_sgd_kernel(T* __restrict__ w, const __grid_constant__ PeerSrcs src, int nsrc, int64_t n,
                                     float lr) {
@@ -466,6 +503,20 @@ int dmt_sgd_dense(void* w, const float* g, int64_t n, float lr, int32_t dtype, d
     case DMT_F64: dmt::sgd_dense_kernel<double><<<grid, 256, 0, s>>>((double*)w, g, n, lr); break;
     default: return DMT_ERR_UNSUPPORTED;
   }
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_peer_barrier(int32_t* epoch, int32_t* const* remote_slots, int32_t* const* local_slots, int32_t n,
+                     int32_t* err, dmt_stream_t stream) {
+  if (n < 0 || n > DMT_MAX_PEER_SRCS || !epoch) return DMT_ERR_SHAPE;
+  dmt::BarrierSlots s{};
+  for (int i = 0; i < n; ++i) {
+    if (!remote_slots[i] || !local_slots[i]) return DMT_ERR_DOMAIN;
+    s.remote[i] = remote_slots[i];
+    s.local[i] = local_slots[i];
+  }
+  dmt::peer_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(epoch, s, n, err);
   DMT_CHECK_LAUNCH();
   return DMT_OK;
 }

@@ -146,6 +146,34 @@ __global__ void slot_offsets_kernel(const int64_t* __restrict__ offsets, int32_t
   if (threadIdx.x == 0) out[num_slots] = carry;
 }
 
+// Step a over NVLink peer stores: the same bundling, but every slot goes
+// straight to its owner's receive buffers (per-slot destination pointers,
+// IPC-mapped for remote owners) -- the all-to-alls of lengths and values
+// become one barrier.  slot_room[s] bounds the slot's values (its fixed
+// capacity); a slot over it ships empty bags like bucketize_kernel.
+struct SlotDst {
+  int32_t* len;
+  int32_t* val;
+  int64_t room;
+};
+
+__global__ void bucketize_peer_kernel(const int32_t* __restrict__ lengths, const int64_t* __restrict__ offsets,
+                                      const int32_t* __restrict__ values, int32_t B,
+                                      const int32_t* __restrict__ slot_feature, const SlotDst* __restrict__ dst) {
+  const int s = blockIdx.y;
+  const int f = slot_feature[s];
+  const SlotDst d = dst[s];
+  const int64_t vbeg = offsets[(int64_t)f * B];
+  const int64_t nnz = offsets[(int64_t)(f + 1) * B] - vbeg;
+  const bool over = nnz > d.room;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B; i += stride)
+    d.len[i] = over ? 0 : lengths[(int64_t)f * B + i];
+  if (over) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride)
+    d.val[i] = __ldg(values + vbeg + i);
+}
+
 // Capacity-padded step a (ragged batches under CUDA graphs): every slot of
 // the send buffer has a fixed capacity, so the step-a splits are static and
 // no count exchange / host sync is needed; the owner then packs each
@@ -224,6 +252,19 @@ int dmt_kjt_bucketize(const int32_t* lengths, const int64_t* offsets, const int3
   dim3 grid(64, num_slots);
   dmt::bucketize_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(lengths, offsets, values, B, slot_feature,
                                                                  slot_value_offset, out_lengths, out_values);
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_kjt_bucketize_peer(const int32_t* lengths, const int64_t* offsets, const int32_t* values, int32_t B,
+                           int32_t num_slots, const int32_t* slot_feature, const void* slot_dst,
+                           dmt_stream_t stream) {
+  if (B < 0 || num_slots < 0) return DMT_ERR_DOMAIN;
+  if (num_slots == 0 || B == 0) return DMT_OK;
+  if (num_slots > 65535) return DMT_ERR_UNSUPPORTED;
+  dim3 grid(64, num_slots);
+  dmt::bucketize_peer_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(lengths, offsets, values, B, slot_feature,
+                                                                      (const dmt::SlotDst*)slot_dst);
   DMT_CHECK_LAUNCH();
   return DMT_OK;
 }

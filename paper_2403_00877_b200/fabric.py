@@ -9,6 +9,7 @@ receiver's buffer is the concatenation of the sources' pieces in group order.
 
 from __future__ import annotations
 
+import os
 from typing import Optional, Sequence
 
 import torch
@@ -174,10 +175,21 @@ class PeerFabric(NcclFabric):
 
     p2p = True
 
+    # barriers of the world / tower / class groups run as device kernels over
+    # NVLink (dmt_peer_barrier); DMT_PEER_BARRIER=nccl keeps the NCCL one
+    device_barrier = os.environ.get("DMT_PEER_BARRIER", "device") == "device"
+
     def __init__(self, world_size: int, rank: int, W: int, backend_device=None):
         super().__init__(world_size, rank, W, backend_device)
         self._flag = torch.zeros(1, dtype=torch.float32, device=self.device)
         self._opened: dict = {}
+        self._bar_args: dict = {}
+        if self.device_barrier and world_size <= 8:
+            # flags[kind][member] (kind 0 world, 1 tower, 2 class) + epochs
+            self._bar_flags = torch.zeros((3, world_size), dtype=torch.int32, device=self.device)
+            self._bar_epoch = torch.zeros(3, dtype=torch.int32, device=self.device)
+            self._bar_err = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self._bar_peers = self.share({"barrier_flags": self._bar_flags})
 
     def share(self, tensors: dict) -> dict:
         """Collective over the world: every rank contributes {name: tensor};
@@ -221,10 +233,39 @@ class PeerFabric(NcclFabric):
             L.lib().dmt_ipc_close(base)
         self._opened.clear()
 
+    def _barrier_kind(self, group) -> Optional[int]:
+        g = tuple(group)
+        r, W = self.rank, self.W
+        if g == tuple(range(self.world_size)):
+            return 0
+        if g == tuple(range((r // W) * W, (r // W + 1) * W)):
+            return 1
+        if g == tuple(t * W + r % W for t in range(self.T)):
+            return 2
+        return None
+
     def barrier_(self, group) -> None:
         """Completion barrier for peer writes: every member's preceding kernels
         (stream order) finished before any member passes it."""
         if len(group) == 1:
+            return
+        kind = self._barrier_kind(group) if self.device_barrier and self.world_size <= 8 else None
+        if kind is not None:
+            import ctypes as C
+
+            from . import _lib as L
+
+            args = self._bar_args.get(kind)
+            if args is None:
+                others = [m for m in group if m != self.rank]
+                es = 4
+                remote = [self._bar_peers[m]["barrier_flags"].data_ptr() + (kind * self.world_size + self.rank) * es
+                          for m in others]
+                local = [self._bar_flags.data_ptr() + (kind * self.world_size + m) * es for m in others]
+                args = ((C.c_void_p * len(others))(*remote), (C.c_void_p * len(others))(*local), len(others))
+                self._bar_args[kind] = args
+            L.check(L.lib().dmt_peer_barrier(self._bar_epoch.data_ptr() + 4 * kind, args[0], args[1], args[2],
+                                             self._bar_err.data_ptr(), L.stream_ptr()), "dmt_peer_barrier")
             return
         self.dist.all_reduce(self._flag, group=self._pg(group))
 

@@ -104,6 +104,14 @@ def kjt_bucketize(lengths, offsets, values, B: int, slot_feature: torch.Tensor,
             "dmt_kjt_bucketize")
 
 
+def kjt_bucketize_peer(lengths, offsets, values, B: int, slot_feature: torch.Tensor, slot_dst: torch.Tensor) -> None:
+    """Step a with every slot written straight into its owner's receive
+    buffers (slot_dst: device table of dmt_slot_dst)."""
+    L.check(L.lib().dmt_kjt_bucketize_peer(lengths.data_ptr(), offsets.data_ptr(), values.data_ptr(), B,
+                                           slot_feature.numel(), slot_feature.data_ptr(), slot_dst.data_ptr(),
+                                           L.stream_ptr()), "dmt_kjt_bucketize_peer")
+
+
 def kjt_slot_offsets(offsets: torch.Tensor, B: int, slot_feature: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
     """Device-side packed slot offsets: out[s+1] - out[s] = nnz of slot s."""
     L.check(L.lib().dmt_kjt_slot_offsets(offsets.data_ptr(), B, slot_feature.numel(), slot_feature.data_ptr(),

@@ -179,6 +179,9 @@ class SpttEngine:
         self.timers: Optional[PhaseTimers] = None
         self.uniform_nnz = False
         self.capacity: Optional[list] = None  # per-feature value capacity (set_capacity)
+        self.p2p_a = False
+        # DMT_PEER_STEP_A=0 keeps step a on NCCL all-to-alls with the peer fabric
+        self.peer_step_a = os.environ.get("DMT_PEER_STEP_A", "1") == "1"
         self._side = None
         self._prepared: dict = {}
         self.p2p_d = self.p2p_f = self.p2p_tm = self.p2p_c = False
@@ -411,8 +414,49 @@ class SpttEngine:
         (host sync; check it outside the timed loop)."""
         return self.capacity is not None and bool(self._cap_flag.item())
 
+    def _init_peer_step_a(self, nnz_pf) -> None:
+        """Step a over NVLink peer stores (uniform or capacity-padded value
+        counts, so every slot's place in its owner's receive buffer is
+        static): persistent receive buffers shared with the world, and the
+        per-slot destination table of dmt_kjt_bucketize_peer.  Collective
+        (every rank calls it in the same step, outside graph capture)."""
+        p, dev = self.plan, self.device
+        (r,) = self.local
+        fpos = lambda sid: p.fpos[p.shards[sid].table_id]
+        C = {o: sum(int(nnz_pf[fpos(sid)]) for sid in p.by_owner[o]) for o in range(p.G)}
+        a_len = torch.empty(max(1, p.owner_bags(r)), dtype=torch.int32, device=dev)
+        a_val = torch.empty(max(1, p.G * C[r]), dtype=torch.int32, device=dev)
+        peers = self.fabric.share({"a_len": a_len, "a_val": a_val})
+        slots = []
+        for o, sid in p.a_slots:
+            k = p.by_owner[o].index(sid)
+            off = sum(int(nnz_pf[fpos(s2)]) for s2 in p.by_owner[o][:k])
+            slots.append(L.SlotDst(len=peers[o]["a_len"].data_ptr() + 4 * (r * p.S[o] + k) * p.B,
+                                   val=peers[o]["a_val"].data_ptr() + 4 * (r * C[o] + off),
+                                   room=int(nnz_pf[fpos(sid)])))
+        self._a_table, _ = K.device_table(L.SlotDst, slots, dev)
+        self._a_bufs = (a_len, a_val)
+        self._a_key = tuple(int(x) for x in nnz_pf)
+        self.p2p_a = True
+
     # ---------------------------------------------------------- forward ----
     def forward(self, kjts: dict, save: bool = False, check_indices: bool = False) -> dict:
+        p, fab, dev = self.plan, self.fabric, self.device
+        world = list(range(p.G))
+        # step a over NVLink peers when every slot's place is static
+        peer_a = (getattr(fab, "p2p", False) and p.G > 1 and len(self.local) == 1 and bool(p.a_slots)
+                  and (self.uniform_nnz or self.capacity is not None) and self.peer_step_a)
+        if peer_a:
+            (r,) = self.local
+            nnz_pf = kjts[r].nnz_per_feature if self.capacity is None else self.capacity
+            if getattr(self, "_a_key", None) != tuple(int(x) for x in nnz_pf):
+                if torch.cuda.is_current_stream_capturing():
+                    raise DomainError("step-a peer buffers must be set up by an eager step before capture")
+                self._init_peer_step_a(nnz_pf)
+            return self._forward_after_a(kjts, save, check_indices, peer_a=True)
+        return self._forward_after_a(kjts, save, check_indices, peer_a=False)
+
+    def _forward_after_a(self, kjts: dict, save: bool, check_indices: bool, peer_a: bool) -> dict:
         p, fab, dev = self.plan, self.fabric, self.device
         world = list(range(p.G))
         # step a: bucketize per src, exchange lengths then values
@@ -425,6 +469,17 @@ class SpttEngine:
             nnz_pf = kj.nnz_per_feature if self.capacity is None else self.capacity
             if self.capacity is not None:
                 K.kjt_check_capacity(offs, p.B, self._cap_dev, self._cap_flag)
+            if peer_a:
+                # every slot straight into its owner's receive buffers, then a
+                # world barrier (replaces the lengths + values all-to-alls)
+                K.kjt_bucketize_peer(kj.lengths, offs, kj.values, p.B, self.slot_feature, self._a_table)
+                if self.trace is not None:
+                    if self.capacity is not None:
+                        self._record_a_device(r, offs, world)
+                    else:
+                        for j, dst in enumerate(world):
+                            self.trace.record_elements("a", r, dst, p.a_send_value_splits(nnz_pf)[j], 4)
+                continue
             slot_offs = p.a_slot_value_offsets(nnz_pf)
             total = slot_offs[-1]
             send_len[r] = torch.empty(max(1, len(p.a_slots) * p.B), dtype=torch.int32, device=dev)
@@ -433,16 +488,17 @@ class SpttEngine:
                 so = K.device_ints(slot_offs, torch.int64, dev)
                 K.kjt_bucketize(kj.lengths, offs, kj.values, p.B, self.slot_feature, so, send_len[r], send_val[r])
                 if self.capacity is not None and self.trace is not None:
-                    # the payload is each slot's actual nnz: device counters
-                    packed = self.buf[r].get("a_slot_packed")
-                    if packed is None:
-                        packed = self.buf[r]["a_slot_packed"] = torch.empty(len(p.a_slots) + 1, dtype=torch.int64,
-                                                                            device=dev)
-                    K.kjt_slot_offsets(offs, p.B, self.slot_feature, packed)
-                    counts = packed[self._owner_slot_end] - packed[self._owner_slot_begin]
-                    self.trace.record_device("a", r, world, counts, 4)
+                    self._record_a_device(r, offs, world)
             len_splits[r] = p.a_send_length_splits()
             val_splits[r] = p.a_send_value_splits(nnz_pf)
+        if peer_a:
+            (r,) = self.local
+            with self._t("exchange_a"):
+                fab.barrier_(world)
+            recv_len, recv_val = {r: self._a_bufs[0]}, {r: self._a_bufs[1]}
+            recv_val_splits = {r: [sum(int(nnz_pf[p.fpos[p.shards[sid].table_id]]) for sid in p.by_owner[r])]
+                               * p.G}
+            return self._forward_from_b(recv_len, recv_val, recv_val_splits, save, check_indices)
         if self.uniform_nnz or self.capacity is not None:
             # fixed pooling factors: every rank ships the same per-feature nnz,
             # so owner r receives val_splits[r][r] from every source and the
@@ -465,6 +521,23 @@ class SpttEngine:
         with self._t("exchange_a"):
             fab.alltoallv(world, "a", send_val, val_splits, recv_val, recv_val_splits,
                           None if self.capacity is not None else self.trace, 4)
+        return self._forward_from_b(recv_len, recv_val, recv_val_splits, save, check_indices)
+
+    def _record_a_device(self, r: int, offs: torch.Tensor, world: list) -> None:
+        """Step-a payload bytes from device counters (capacity mode: the host
+        only knows capacities; each slot ships its actual nnz)."""
+        p = self.plan
+        packed = self.buf[r].get("a_slot_packed")
+        if packed is None:
+            packed = self.buf[r]["a_slot_packed"] = torch.empty(len(p.a_slots) + 1, dtype=torch.int64,
+                                                                device=self.device)
+        K.kjt_slot_offsets(offs, p.B, self.slot_feature, packed)
+        counts = packed[self._owner_slot_end] - packed[self._owner_slot_begin]
+        self.trace.record_device("a", r, world, counts, 4)
+
+    def _forward_from_b(self, recv_len: dict, recv_val: dict, recv_val_splits: dict, save: bool,
+                        check_indices: bool) -> dict:
+        p, fab, dev = self.plan, self.fabric, self.device
         # step b: lookup (+ fused permute) on every owner
         self._owner = {}
         err = torch.zeros(1, dtype=torch.int32, device=dev) if check_indices else None

@@ -50,7 +50,7 @@ def _build(hosts, rph, dev, tm_kind="dcn"):
     return topo, layout, placement, assignment, pooling, cfg, kjts, B
 
 
-def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1, tm_kind="dcn", mode="sptt"):
+def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1, tm_kind="dcn", mode="sptt", capacity=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
 
@@ -74,6 +74,10 @@ def _worker(rank, world, port, hosts, rph, q, kind="nccl", steps=1, tm_kind="dcn
         topo2, layout2, placement2, _, _, _, kjts2, _ = _build(hosts, rph, dev, tm_kind)
         ref = SPTT(topo2, layout2, placement2, assignment, pooling, B, LoopbackFabric(world, dev), tm=cfg,
                    dtype=torch.float32, device=dev, lr=0.005, mode=mode)
+        if capacity:  # capacity-padded step a (peer fabric: straight into the owners' buffers)
+            caps = [max(kjts[r].nnz_per_feature[f] for r in range(world)) + 3 for f in range(len(pooling))]
+            dist_model.set_capacity(caps)
+            ref.set_capacity(caps)
         gen = np.random.default_rng(5)
         O = dist_model.out_width
         grads = {r: torch.from_numpy(gen.normal(size=(B, O)).astype(np.float32)).to(dev) for r in range(world)}
@@ -170,6 +174,32 @@ def test_distributed_flat_baseline_matches_loopback(hosts, rph, kind):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, hosts, rph, q, kind, 3, "dcn", "flat"))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, err in res:
+        assert ok, f"rank {rank}: {err}"
+
+
+@pytest.mark.parametrize("kind", ["nccl", "peer"])
+@pytest.mark.parametrize("hosts,rph", [(2, 2), (4, 1)])
+def test_distributed_capacity_padded_step_a(hosts, rph, kind):
+    """Ragged batches through the capacity-padded step a (static splits; on
+    the peer fabric the bucketize stores every slot straight into its owner's
+    receive buffers, one barrier instead of two all-to-alls): bit-identical
+    to the loopback engine."""
+    world = hosts * rph
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, hosts, rph, q, kind, 3, "dcn", "sptt", True))
              for r in range(world)]
     for p in procs:
         p.start()
