@@ -253,6 +253,8 @@ enum dmt_epilogue {
 };
 
 #define DMT_GEMM_MAX_PAIRS 4
+#define DMT_GEMM_MAX_OUT_GROUPS 8
+#define DMT_GEMM_MAX_COL_GROUPS 32
 
 /* dmt_gemm_args.flags: operand stored transposed (MN-major).  TRANS_A: `a`
  * holds A^T as a [k, m] matrix with row stride lda (m contiguous); TRANS_B:
@@ -309,8 +311,23 @@ typedef struct dmt_gemm_args {
    * separate CTAs into splitk_ws (fp32, ksplit * m * n), then summed in split
    * order (deterministic) with the NONE / ACC epilogue applied.  0/1 = off. */
   int32_t ksplit;
-  int32_t pad2_;
+  /* scattered output rows (a GEMM fused with the exchange that follows it):
+   * with n_out_groups > 0, row m goes to out_group[m / rows_per_group] +
+   * (m % rows_per_group) * ld_d -- e.g. the tower module's projection writes
+   * each destination tower's block straight into that rank's step-f receive
+   * buffer over NVLink (peer-mapped pointers). */
+  int32_t n_out_groups;
   float* splitk_ws;
+  void* out_group[DMT_GEMM_MAX_OUT_GROUPS];
+  /* scattered output column blocks: with n_col_groups > 0, column n goes to
+   * col_group[n / col_group_width] + m * col_group_ld[g] + n % width -- e.g.
+   * the DCN backward's final dX GEMM stores each shard's columns straight into
+   * its owner's gradient buffer over NVLink (step d^-1 fused); width a
+   * multiple of 32 covering n exactly. */
+  int32_t n_col_groups;
+  int32_t col_group_width;
+  void* col_group[DMT_GEMM_MAX_COL_GROUPS];
+  int64_t col_group_ld[DMT_GEMM_MAX_COL_GROUPS];
 } dmt_gemm_args;
 
 /* rows of the colsum_part buffer for an m-row GEMM */

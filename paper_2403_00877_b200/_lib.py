@@ -23,6 +23,8 @@ EPI_BIAS_RELU, EPI_RELU_BWD = 6, 7
 GEMM_TRANS_A, GEMM_TRANS_B, GEMM_AUX2_ACCUM, GEMM_SCALE_ACC = 1, 2, 4, 8
 GEMM_NO_PREFETCH, GEMM_BN_SHIFT, GEMM_CLUSTER, GEMM_SINGLE_CTA = 16, 8, 32, 64  # tuning overrides
 GEMM_MAX_PAIRS = 4
+GEMM_MAX_OUT_GROUPS = 8
+GEMM_MAX_COL_GROUPS = 32
 MAX_PEER_SRCS = 8  # DMT_MAX_PEER_SRCS (include/dmt.h)
 OPT_SGD, OPT_ROWWISE_ADAGRAD = 0, 1
 EBIT_INDEX, EBIT_BAGLEN = 1, 2
@@ -70,7 +72,10 @@ class GemmArgs(C.Structure):
         ("rows_per_group", i64), ("ld_group", i64),
         ("beta", f32), ("alpha", f32), ("in_dtype", i32), ("out_dtype", i32), ("epilogue", i32), ("flags", i32),
         ("npairs", i32), ("pad_", i32), ("pair_g", vp * GEMM_MAX_PAIRS), ("pair_u", vp * GEMM_MAX_PAIRS),
-        ("colsum_part", vp), ("ksplit", i32), ("pad2_", i32), ("splitk_ws", vp),
+        ("colsum_part", vp), ("ksplit", i32), ("n_out_groups", i32), ("splitk_ws", vp),
+        ("out_group", vp * GEMM_MAX_OUT_GROUPS),
+        ("n_col_groups", i32), ("col_group_width", i32), ("col_group", vp * GEMM_MAX_COL_GROUPS),
+        ("col_group_ld", i64 * GEMM_MAX_COL_GROUPS),
     ]
 
 

@@ -178,6 +178,22 @@ int dmt_gemm_ex(const dmt_gemm_args* args, const void* a_lo, const void* b_lo, d
   if ((a->epilogue == DMT_EPI_DCN_BWD || a->epilogue == DMT_EPI_DCN_FINAL) && a->out_dtype != a->in_dtype)
     return DMT_ERR_UNSUPPORTED;
   if (a->epilogue > DMT_EPI_RELU_BWD || a->epilogue < 0) return DMT_ERR_DOMAIN;
+  if (a->n_out_groups < 0 || a->n_out_groups > DMT_GEMM_MAX_OUT_GROUPS) return DMT_ERR_DOMAIN;
+  if (a->n_col_groups < 0 || a->n_col_groups > DMT_GEMM_MAX_COL_GROUPS) return DMT_ERR_DOMAIN;
+  if (a->n_col_groups) {
+    if (a->n_out_groups || a->ksplit > 1 || a->col_group_width <= 0 || a->col_group_width % 32 ||
+        (int64_t)a->n_col_groups * a->col_group_width != a->n || a->rows_per_group > 0)
+      return DMT_ERR_DOMAIN;
+    for (int j = 0; j < a->n_col_groups; ++j)
+      if (!a->col_group[j] || a->col_group_ld[j] < a->col_group_width) return DMT_ERR_DOMAIN;
+  }
+  if (a->n_out_groups) {
+    if (a->rows_per_group <= 0 || (a->m + a->rows_per_group - 1) / a->rows_per_group > a->n_out_groups ||
+        a->ksplit > 1 || a->colsum_part)
+      return DMT_ERR_DOMAIN;
+    for (int j = 0; j < a->n_out_groups; ++j)
+      if (!a->out_group[j]) return DMT_ERR_DOMAIN;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   if (a->ksplit > 1) {
     if (!a->splitk_ws || (a->epilogue != DMT_EPI_NONE && a->epilogue != DMT_EPI_ACC) ||

@@ -305,6 +305,12 @@ struct Params {
   const void* pu[DMT_GEMM_MAX_PAIRS];
   float* colsum;  // DCN_BWD: per (128-row tile, 32-row quarter) column sums of the stored gu
   int kchunk;     // tf32: K blocks accumulated per TMEM chunk (see gemm_kernel)
+  int ngroups_out;  // > 0: row m -> gout[m / rows_per_group] + (m % rows_per_group) * ld_d
+  void* gout[DMT_GEMM_MAX_OUT_GROUPS];
+  int ncolg;        // > 0: column n -> colg[n / colg_w] + m * colg_ld[g] + n % colg_w
+  int colg_w;
+  void* colg[DMT_GEMM_MAX_COL_GROUPS];
+  int64_t colg_ld[DMT_GEMM_MAX_COL_GROUPS];
   int ksplit;     // split-K: units = tiles x ksplit; split s covers K blocks [s*kbs, (s+1)*kbs)
   int kbs;        //   and writes its raw fp32 accumulator at output rows + s * m (workspace)
 };
@@ -316,8 +322,22 @@ struct Params {
 template <typename TO>
 __device__ __forceinline__ TO* out_row(const Params& p, int64_t row) {
   TO* d = reinterpret_cast<TO*>(p.d);
+  if (p.ngroups_out)  // scattered row blocks (peer step-f receive buffers)
+    return reinterpret_cast<TO*>(p.gout[row / p.rows_per_group]) + (row % p.rows_per_group) * p.ld_d;
   if (p.rows_per_group > p.m) return d + row * p.ld_d;
   return d + (row / p.rows_per_group) * p.ld_group + (row % p.rows_per_group) * p.ld_d;
+}
+
+// Address of output element (row, col): the plain / grouped-row layouts, or a
+// scattered column block (the dX GEMM storing shards into their owners'
+// gradient buffers).  A 32-column chunk never straddles a column block.
+template <typename TO>
+__device__ __forceinline__ TO* out_ptr(const Params& p, int64_t row, int64_t col) {
+  if (p.ncolg) {
+    const int g = (int)(col / p.colg_w);
+    return reinterpret_cast<TO*>(p.colg[g]) + row * p.colg_ld[g] + (col - (int64_t)g * p.colg_w);
+  }
+  return out_row<TO>(p, row) + col;
 }
 
 // 32 consecutive elements of one row <-> 32 fp32 registers.  The vector forms
@@ -442,8 +462,7 @@ __device__ __forceinline__ void epi8(const Params& p, int64_t row, int64_t col, 
       store8<float>(p.aux2 + xo, d);
     }
   }
-  TO* drow = out_row<TO>(p, row);
-  store8<TO>(drow + col, v);
+  store8<TO>(out_ptr<TO>(p, row, col), v);
 }
 
 // Raw (unconverted) epilogue inputs of one 8-column row piece, so two pieces'
@@ -571,8 +590,7 @@ __device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t
       }
     }
   }
-  TO* drow = out_row<TO>(p, row + soff);  // soff: split-K workspace rows
-  store8<TO>(drow + col, v);
+  store8<TO>(out_ptr<TO>(p, row + soff, col), v);  // soff: split-K workspace rows
 }
 
 // The epilogue operands of a tile (x0 / xl / C / dx0 blocks) do not depend on
@@ -911,9 +929,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       tc_fence_after();
       const int64_t row = m0 + q * 32 + lane;
       const bool row_ok = row < p.m;
-      TO* drow = nullptr;
-      if (row_ok)
-        drow = out_row<TO>(p, row + soff);
 #pragma unroll 1
       for (int c = half * kColsPerWarp; c < (half + 1) * kColsPerWarp; c += 32) {
         float v[32];
@@ -1073,8 +1088,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             }
           }
         }
-        if (full && p.vec_store) store32v<TO>(drow + col, v);
-        else store32s<TO>(drow + col, v, ncols);
+        if (full && p.vec_store) store32v<TO>(out_ptr<TO>(p, row + soff, col), v);
+        else store32s<TO>(out_ptr<TO>(p, row + soff, col), v, ncols);
       }
       tc_fence_before();
       __syncwarp();
@@ -1228,6 +1243,19 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   p.beta = a->beta; p.out_dtype = a->out_dtype; p.in_dtype = a->in_dtype; p.epilogue = a->epilogue;
   size_t eo = dtype_size(a->out_dtype);
   p.vec_store = ((uintptr_t)a->d % 16 == 0) && ((a->ld_d * eo) % 16 == 0) && ((a->ld_group * eo) % 16 == 0);
+  p.ngroups_out = a->n_out_groups;
+  p.ncolg = a->n_col_groups;
+  p.colg_w = a->col_group_width > 0 ? a->col_group_width : 1;
+  for (int j = 0; j < DMT_GEMM_MAX_COL_GROUPS; ++j) {
+    p.colg[j] = j < a->n_col_groups ? a->col_group[j] : nullptr;
+    p.colg_ld[j] = j < a->n_col_groups ? a->col_group_ld[j] : 0;
+    if (j < a->n_col_groups)
+      p.vec_store = p.vec_store && ((uintptr_t)a->col_group[j] % 16 == 0) && ((a->col_group_ld[j] * eo) % 16 == 0);
+  }
+  for (int j = 0; j < DMT_GEMM_MAX_OUT_GROUPS; ++j) {
+    p.gout[j] = j < a->n_out_groups ? a->out_group[j] : nullptr;
+    if (j < a->n_out_groups) p.vec_store = p.vec_store && ((uintptr_t)a->out_group[j] % 16 == 0);
+  }
   size_t ei = dtype_size(a->in_dtype);
   p.vec_x = ((uintptr_t)a->x0 % 16 == 0) && ((uintptr_t)a->xl % 16 == 0) && ((uintptr_t)a->aux % 16 == 0) &&
             ((uintptr_t)a->aux2 % 16 == 0) && ((a->ld_x * ei) % 16 == 0) && ((a->ld_x * 4) % 16 == 0);

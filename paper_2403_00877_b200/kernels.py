@@ -371,14 +371,20 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[
          rows_per_group: int = 0, ld_group: int = 0, ld_d: Optional[int] = None,
          b_split=None, trans_a: bool = False, trans_b: bool = False, c=None, aux2=None,
          aux2_accum: bool = False, alpha: Optional[float] = None, tune_flags: int = 0,
-         pairs=(), colsum_part: Optional[torch.Tensor] = None) -> torch.Tensor:
+         pairs=(), colsum_part: Optional[torch.Tensor] = None, out_groups: Sequence[int] = (),
+         col_groups: Sequence[tuple] = (), col_group_width: int = 0) -> torch.Tensor:
     """out[m, n] = epi(sum_k A[m, k] B[n, k]) on tcgen05 (bf16/f16 -> kind::f16,
     fp32 -> 3xTF32).  A = a (m, k), or a^T when ``trans_a`` (a stored (k, m));
     B = b (n, k), or b^T when ``trans_b`` (b stored (k, n)).  Transposed
     operands are read MN-major by TMA (no transpose pass).  ``b_split`` may
     carry a cached (hi, lo) tf32 split of an fp32 b.  ``pairs`` [(g, u), ...]
     adds sum g*u in the DCN_FINAL epilogue; ``colsum_part`` receives the fused
-    per-tile column sums of gu (DCN_BWD; finish with column_sum_parts)."""
+    per-tile column sums of gu (DCN_BWD; finish with column_sum_parts).
+    ``out_groups`` (device addresses, with ``rows_per_group``): row block j is
+    stored at out_groups[j] (row stride ld_d) instead of into ``out`` -- the
+    GEMM fused with a scatter to peers' buffers.  ``col_groups`` [(address,
+    row stride)] with ``col_group_width``: column block g is stored at its own
+    address instead (the dX GEMM scattering shards to their owners)."""
     if a.dim() != 2 or b.dim() != 2:
         raise ShapeError("gemm operands must be 2-D")
     m, k = (a.shape[1], a.shape[0]) if trans_a else (a.shape[0], a.shape[1])
@@ -437,6 +443,20 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, bias: Optional[
         args.splitk_ws = ws.data_ptr()
     for j, (g, u) in enumerate(pairs):
         args.pair_g[j], args.pair_u[j] = g.data_ptr(), u.data_ptr()
+    if col_groups:
+        if len(col_groups) > L.GEMM_MAX_COL_GROUPS or col_group_width * len(col_groups) != n:
+            raise DomainError("col_groups must tile the output columns (at most 32 blocks)")
+        args.n_col_groups = len(col_groups)
+        args.col_group_width = col_group_width
+        for j, (ptr, ld) in enumerate(col_groups):
+            args.col_group[j] = int(ptr)
+            args.col_group_ld[j] = int(ld)
+    if out_groups:
+        if len(out_groups) > L.GEMM_MAX_OUT_GROUPS or not rows_per_group:
+            raise DomainError("out_groups needs rows_per_group and at most 8 groups")
+        args.n_out_groups = len(out_groups)
+        for j, ptr in enumerate(out_groups):
+            args.out_group[j] = int(ptr)
     L.check(L.lib().dmt_gemm_ex(C.byref(args), L.ptr(a_lo), L.ptr(b_lo), L.stream_ptr()), "dmt_gemm")
     return out
 

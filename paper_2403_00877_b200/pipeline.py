@@ -105,6 +105,11 @@ class KJT:
         return self.offsets
 
 
+def p_unsupported(plan) -> bool:
+    """Step-f fusion needs at most DMT_GEMM_MAX_OUT_GROUPS towers."""
+    return plan.T > L.GEMM_MAX_OUT_GROUPS
+
+
 class SpttEngine:
     def __init__(self, plan: ExchangePlan, placement: ShardedEmbedding, fabric: Fabric, dtype: torch.dtype,
                  device=None, tower_modules: Optional[dict] = None, mode: str = "sptt",
@@ -180,6 +185,11 @@ class SpttEngine:
         self.uniform_nnz = False
         self.capacity: Optional[list] = None  # per-feature value capacity (set_capacity)
         self.p2p_a = False
+        # DMT_FUSE_F=0 / DMT_FUSE_D_BWD=0: keep step f / d^-1 as separate
+        # peer-copy launches instead of fusing them into the TM GEMM epilogues
+        self.fuse_f = os.environ.get("DMT_FUSE_F", "1") == "1"
+        self.fuse_d_bwd = os.environ.get("DMT_FUSE_D_BWD", "1") == "1"
+        self.c_bwd_fused = False
         # DMT_PEER_STEP_A=0 keeps step a on NCCL all-to-alls with the peer fabric
         self.peer_step_a = os.environ.get("DMT_PEER_STEP_A", "1") == "1"
         self._side = None
@@ -261,6 +271,68 @@ class SpttEngine:
                                   row_begin=seg.row_begin, row_filter=seg.row_filter, key_base=seg.key_base,
                                   table_rows=seg.table_rows))
         self.seg_fwd_p2p = K.SegmentTable(segs, dev)
+
+    def flat_dx_scatter(self, r: int):
+        """The flat baseline's c^-1 as a column scatter of the global TM's dX
+        GEMM (see _d_bwd_fused_scatter); None unless fusable."""
+        if not (self.p2p_c and self.fuse_d_bwd):
+            return None
+        p = self.plan
+        groups, col, width = [], 0, None
+        for fb in p.c_blocks():
+            for pc in fb.pieces:
+                if fb.rowwise or fb.dst_col + pc.c0 != col:
+                    return None
+                width = width or pc.width
+                if pc.width != width or pc.ld != width:
+                    return None
+                o = self.placement.shards[pc.sid].rank
+                k = p.k_of(pc.sid)
+                off = r * p.B * p.SW[o] + p.B * p.pre[o][k]
+                groups.append((self.peer[o]["grad_x"].data_ptr() + off * self.es, pc.ld))
+                col += pc.width
+        if not groups or width % 32 or len(groups) > L.GEMM_MAX_COL_GROUPS or col != p.flat_width():
+            return None
+        return width, groups
+
+    def _d_bwd_fused_scatter(self, r: int):
+        """(width, [(owner gradient-buffer address, row stride)] per dX column
+        block) for the DCN's final dX GEMM to store d^-1 straight into the
+        owners over NVLink; None unless every piece has one width (a multiple
+        of 32) and the pieces tile X's columns in order."""
+        if not self.fuse_d_bwd:
+            return None
+        p = self.plan
+        c = r % p.W
+        groups, col, width = [], 0, None
+        for fb in p.e_blocks(r):
+            for pc in fb.pieces:
+                if fb.rowwise or fb.dst_col + pc.c0 != col:
+                    return None
+                if width is None:
+                    width = pc.width
+                if pc.width != width or pc.ld != width:
+                    return None
+                o = self.placement.shards[pc.sid].rank
+                k = p.k_of(pc.sid)
+                off = c * p.T * p.B * p.SW[o] + p.T * p.B * p.pre[o][k]
+                groups.append((self.peer[o]["grad_x"].data_ptr() + off * self.es, pc.ld))
+                col += pc.width
+        if not groups or width % 32 or len(groups) > L.GEMM_MAX_COL_GROUPS or col != p.x_width(r):
+            return None
+        return width, groups
+
+    def _f_fused_groups(self, r: int):
+        """(B, [address of block j in the tower-j class member's step-f receive
+        buffer]) for the TM projection GEMM to store into directly over NVLink
+        (step f fused into the GEMM epilogue); None when not applicable."""
+        if not self.fuse_f or p_unsupported(self.plan):
+            return None
+        p = self.plan
+        t, c = p.tower_of(r), r % p.W
+        es = self.es
+        off_recv = p.B * sum(p.O[t2] for t2 in range(t))
+        return p.B, [self.peer[j * p.W + c]["recv_f"].data_ptr() + off_recv * es for j in range(p.T)]
 
     def _f_peer_copies(self, r: int) -> K.CopyTable:
         """Step f: Y block j -> the class member in tower j (its recv_f slot)."""
@@ -584,8 +656,9 @@ class SpttEngine:
                 self.asm_e[r].run()
             t = p.tower_of(r)
             if t in self.tm:
+                groups = self._f_fused_groups(r) if (self.p2p_f and self.tm[t].cfg.kind == "dcn") else None
                 with self._t("tm_fwd"):
-                    self.tm[t].forward(self.buf[r]["X"], save=save, out=self.buf[r]["Y"])
+                    self.tm[t].forward(self.buf[r]["X"], save=save, out=self.buf[r]["Y"], out_groups=groups)
                 if save:
                     self.buf[r]["tm_saved"] = self.tm[t]._saved
         # step f: per-class all-to-alls, then tower-grouped output
@@ -596,9 +669,11 @@ class SpttEngine:
                 (r,) = self.local
                 self._record_f(r)
                 with self._t("exchange_f"):
-                    if "f_copies" not in self.buf[r]:
-                        self.buf[r]["f_copies"] = self._f_peer_copies(r)
-                    self.buf[r]["f_copies"].run()  # peer stores over NVLink
+                    if not self._f_fused_groups(r) or p.tower_of(r) not in self.tm or \
+                            self.tm[p.tower_of(r)].cfg.kind != "dcn":
+                        if "f_copies" not in self.buf[r]:
+                            self.buf[r]["f_copies"] = self._f_peer_copies(r)
+                        self.buf[r]["f_copies"].run()  # peer stores over NVLink
                     fab.barrier_(g)
                 continue
             with self._t("exchange_f"):
@@ -722,9 +797,12 @@ class SpttEngine:
                 # a one-rank tower needs no gradient all-reduce: fuse the weight
                 # SGD into the dW GEMM epilogues
                 fused = (tm_lr if tm_lr is not None else lr) if p.W == 1 else None
+                scatter = self._d_bwd_fused_scatter(r) if (self.p2p_d and self.tm[t].cfg.kind == "dcn") else None
                 with self._t("tm_bwd"):
                     dX[r] = self.tm[t].backward(grecv[r], fused_lr=fused,
-                                                dx_out=self.buf[r]["gX"] if self.direct_x.get(r) else None)
+                                                dx_out=self.buf[r]["gX"] if self.direct_x.get(r) else None,
+                                                dx_scatter=scatter)
+                self._d_bwd_fused = scatter is not None and self.tm[t]._dx_scatter is not None
                 acc = tower_grads.setdefault(t, {})
                 for k, v in self.tm[t].grads.items():
                     if self.p2p_tm:  # one rank per process: into the peer-shared buffer
@@ -738,6 +816,10 @@ class SpttEngine:
         for r in self.local:
             if self.direct_x.get(r):
                 continue  # the embedding backward reads gX directly
+            if self.p2p_d and getattr(self, "_d_bwd_fused", False):
+                with self._t("exchange_d_bwd"):  # the dX GEMM already stored every block
+                    fab.barrier_(p.group_of(r))
+                continue
             if self.p2p_d:
                 # d^-1 over NVLink: scatter dX columns straight into every
                 # owner's gradient buffer (its step-d send layout, member block c)
@@ -823,6 +905,15 @@ class SpttEngine:
         world = list(range(p.G))
         gsend = {}
         fw = p.flat_width()
+        if self.p2p_c and self.c_bwd_fused:
+            self.c_bwd_fused = False
+            with self._t("exchange_c_bwd"):  # the global TM's dX GEMM already stored every block
+                fab.barrier_(world)
+            if dense_hook is None:
+                self._embedding_update(lr, optimizer, eps)
+            else:
+                self.overlap_with_embedding_update(dense_hook, lr, optimizer, eps)
+            return
         if self.p2p_c:
             # c^-1 over NVLink: each feature block of this rank's output
             # gradient goes straight into its owner's gradient buffer (the

@@ -132,8 +132,12 @@ class SPTT:
         dx, acc = {}, {}
         for r, g in grads.items():
             self.global_tm._saved = self._gsaved[r]
+            # peer fabric: the global TM's dX GEMM stores step c^-1 straight
+            # into the owners' gradient buffers (same fusion as SPTT's d^-1)
+            scatter = self.engine.flat_dx_scatter(r)
             with self.engine._t("tm_bwd"):
-                dx[r] = self.global_tm.backward(g)
+                dx[r] = self.global_tm.backward(g, dx_scatter=scatter)
+            self.engine.c_bwd_fused = scatter is not None and self.global_tm._dx_scatter is not None
             for k, v in self.global_tm.grads.items():
                 acc[k] = v.clone() if k not in acc else acc[k].add_(v)
 

@@ -187,7 +187,12 @@ class TowerModule:
         self._saved = None
 
     # -- forward ---------------------------------------------------------------
-    def forward(self, x: torch.Tensor, save: bool = False, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, save: bool = False, out: Optional[torch.Tensor] = None,
+                out_groups: Optional[tuple] = None) -> torch.Tensor:
+        """``out_groups`` = (rows_per_group, [device addresses]): a DCN module's
+        projection GEMM stores row block j straight at address j (row stride =
+        the output width) -- step f fused into the TM (peer receive buffers);
+        ``out`` then only supplies the dtype."""
         rows = x.shape[0]
         if x.dim() != 2 or x.shape[1] != self.F * self.N:
             raise ShapeError(f"TM input {tuple(x.shape)} != (rows, {self.F * self.N})")
@@ -213,7 +218,12 @@ class TowerModule:
                 us.append(u)
                 xs.append(nxt)
             xl = nxt
-        K.gemm(xl, self.w["w_proj"], y, bias=self.w["b_proj"], epilogue=L.EPI_BIAS)
+        if out_groups is not None:
+            rpg, ptrs = out_groups
+            K.gemm(xl, self.w["w_proj"], y, bias=self.w["b_proj"], epilogue=L.EPI_BIAS, rows_per_group=rpg,
+                   ld_d=self.width, out_groups=ptrs)
+        else:
+            K.gemm(xl, self.w["w_proj"], y, bias=self.w["b_proj"], epilogue=L.EPI_BIAS)
         if save:
             self._saved = (xs, us)
         return y
@@ -235,7 +245,7 @@ class TowerModule:
 
     # -- backward --------------------------------------------------------------
     def backward(self, gy: torch.Tensor, fused_lr: Optional[float] = None,
-                 dx_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                 dx_out: Optional[torch.Tensor] = None, dx_scatter: Optional[tuple] = None) -> torch.Tensor:
         """Returns dX (rows, F*N) in the compute dtype; fp32 weight grads are
         stored in ``self.grads`` (this rank's contribution only).
 
@@ -247,6 +257,9 @@ class TowerModule:
         if self._saved is None:
             raise DomainError("backward() needs forward(save=True)")
         self._dx_out = dx_out
+        # (width, [(address, row stride)]): the DCN's final dX GEMM stores each
+        # column block straight there (step d^-1 fused; accumulate form only)
+        self._dx_scatter = dx_scatter if (self.cfg.kind == DCN and self.dcn_bwd_form != "pairs") else None
         if self.cfg.kind == DLRM:
             return self._dlrm_bwd(gy)
         return self._dcn_bwd(gy, fused_lr)
@@ -350,7 +363,9 @@ class TowerModule:
                 K.gemm(cur, self.w[f"w{layer}"], g, trans_b=True, epilogue=L.EPI_DCN_BWD, c=g, beta=1.0, x0=x0,
                        xl=us[layer - 1], aux=gu[(layer - 1) % 2], aux2=dx0, aux2_accum=True, colsum_part=part)
             else:
-                K.gemm(cur, self.w["w0"], dx, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=g, beta=1.0, aux2=dx0)
+                sc = self._dx_scatter
+                K.gemm(cur, self.w["w0"], dx, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=g, beta=1.0, aux2=dx0,
+                       col_groups=sc[1] if sc else (), col_group_width=sc[0] if sc else 0)
             weight_grad(f"w{layer}", cur, xs[layer])
         return dx
 

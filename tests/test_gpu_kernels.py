@@ -341,3 +341,38 @@ def test_gemm_splitk_weight_grads(dt, m, n, k):
     ww = 1.0 - 1e-3 * want
     ulp = 2.0 ** -8 if dt == torch.bfloat16 else 2.0 ** -23
     assert ((w.double() - ww).abs() <= ulp + tol * 1e-3 * mag).all()
+
+
+@pytest.mark.parametrize("pair", [False, True])
+def test_gemm_scattered_row_and_column_groups(pair):
+    """Output scatter used to fuse the exchanges into the tower-module GEMMs:
+    row blocks to separate buffers (step f from the projection) and column
+    blocks to separate buffers with their own row strides (d^-1 from the
+    final dX GEMM) -- bit-identical to the plain GEMM's output blocks."""
+    from paper_2403_00877_b200 import _lib as L
+    from paper_2403_00877_b200 import kernels as K
+
+    dt = torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(9)
+    m, n, k, rpg = 1024, 512, 256, 256
+    a = torch.randn(m, k, device="cuda", generator=g).to(dt)
+    b = (torch.randn(n, k, device="cuda", generator=g) / 16).to(dt)
+    bias = torch.randn(n, device="cuda", generator=g)
+    fl = L.GEMM_CLUSTER if pair else L.GEMM_SINGLE_CTA
+    want = torch.empty(m, n, device="cuda", dtype=dt)
+    K.gemm(a, b, want, bias=bias, epilogue=L.EPI_BIAS, tune_flags=fl)
+    rows = [torch.zeros(rpg + 3, n, device="cuda", dtype=dt) for _ in range(m // rpg)]
+    K.gemm(a, b, want, bias=bias, epilogue=L.EPI_BIAS, tune_flags=fl, rows_per_group=rpg, ld_d=n,
+           out_groups=[t.data_ptr() + 3 * n * 2 for t in rows])
+    cols = [torch.zeros(m, 128 + 64 * j, device="cuda", dtype=dt) for j in range(n // 128)]
+    x0 = torch.randn(m, n, device="cuda", generator=g).to(dt)
+    d0 = torch.randn(m, n, device="cuda", generator=g)
+    want2 = torch.empty(m, n, device="cuda", dtype=dt)
+    K.gemm(a, b, want2, epilogue=L.EPI_DCN_FINAL, c=x0, beta=1.0, aux2=d0, tune_flags=fl)
+    K.gemm(a, b, want2.clone(), epilogue=L.EPI_DCN_FINAL, c=x0, beta=1.0, aux2=d0, tune_flags=fl,
+           col_groups=[(t.data_ptr(), t.stride(0)) for t in cols], col_group_width=128)
+    torch.cuda.synchronize()
+    for j, t in enumerate(rows):
+        assert torch.equal(t[3:], want[j * rpg:(j + 1) * rpg])
+    for j, t in enumerate(cols):
+        assert torch.equal(t[:, :128], want2[:, j * 128:(j + 1) * 128])
