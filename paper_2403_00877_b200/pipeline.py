@@ -105,7 +105,7 @@ class KJT:
         return self.offsets
 
 
-def p_unsupported(plan) -> bool:
+def _too_many_towers(plan) -> bool:
     """Step-f fusion needs at most DMT_GEMM_MAX_OUT_GROUPS towers."""
     return plan.T > L.GEMM_MAX_OUT_GROUPS
 
@@ -326,7 +326,7 @@ class SpttEngine:
         """(B, [address of block j in the tower-j class member's step-f receive
         buffer]) for the TM projection GEMM to store into directly over NVLink
         (step f fused into the GEMM epilogue); None when not applicable."""
-        if not self.fuse_f or p_unsupported(self.plan):
+        if not self.fuse_f or _too_many_towers(self.plan):
             return None
         p = self.plan
         t, c = p.tower_of(r), r % p.W
