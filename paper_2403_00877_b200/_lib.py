@@ -14,7 +14,7 @@ import torch
 from .errors import STATUS_ERRORS, TowersimError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdmt.so")
+LIB_PATH = os.environ.get("DMT_LIB", os.path.join(_HERE, "libdmt.so"))  # DMT_LIB: A/B builds
 
 DT_F32, DT_BF16, DT_F64, DT_F16 = 0, 1, 2, 3
 POOL_NONE, POOL_SUM, POOL_MEAN = 0, 1, 2
