@@ -155,7 +155,8 @@ class SpttEngine:
                 # singleton class (T = 1): step f is the identity -> alias
                 b["recv_f"] = (b["Y"].view(-1) if p.T == 1 else
                                torch.empty(max(1, sum(p.f_recv_splits(r))), dtype=dtype, device=dev))
-                b["out"] = torch.empty((p.B, p.out_width()), dtype=dtype, device=dev)
+                # one tower: the tower-grouped output IS Y (no output gather)
+                b["out"] = b["Y"] if p.T == 1 else torch.empty((p.B, p.out_width()), dtype=dtype, device=dev)
             else:
                 b["recv_c"] = (b["send_x"] if p.G == 1 else
                                torch.empty(max(1, sum(p.c_recv_splits(r))), dtype=dtype, device=dev))
@@ -681,7 +682,8 @@ class SpttEngine:
                               {r: p.f_recv_splits(r) for r in g}, self.trace, self.es)
         out = {}
         for r in self.local:
-            self.asm_out[r].run()
+            if self.buf[r]["out"] is not self.buf[r]["Y"]:
+                self.asm_out[r].run()
             out[r] = self.buf[r]["out"]
         return out
 
@@ -770,6 +772,11 @@ class SpttEngine:
                     K.Copy2DTable(copies, dev).run()
                     fab.barrier_(p.class_group_of(r))
                 grecv[r] = self.buf[r]["g_y"]
+                continue
+            go = grad_out[r]
+            if p.T == 1 and go.is_contiguous() and tuple(go.shape) == (p.B, p.O[p.tower_of(r)]):
+                # one tower: the output gradient already is the TM's gy layout
+                gsend[r], grecv[r] = go.view(-1), go
                 continue
             gf = self._persist(r, "g_f", self.buf[r]["recv_f"])
             copies = []
