@@ -360,6 +360,13 @@ int dmt_column_sum(const void* in, int64_t rows, int64_t cols, int64_t ld, float
 int dmt_cross_bwd_pointwise(const void* g, const void* x0, const void* u, void* gu, float* dx0,
                             int64_t n, int32_t dtype, dmt_stream_t stream);
 
+/* dx0 = (accumulate ? dx0 : 0) + g * u  (g, u in dtype; dx0 fp32; n elements,
+ * 16-byte aligned): one term of the crossnet's dx0 = sum_l g_{l+1} * u_l
+ * (derivative of towermod.py:132-139), run on a side stream beside the dW
+ * GEMMs so the dX GEMM epilogues stay light. */
+int dmt_dcn_dx0_term(const void* g, const void* u, float* dx0, int64_t n, int32_t dtype, int32_t accumulate,
+                     dmt_stream_t stream);
+
 /* w -= lr * g  (w in dtype, g fp32), n elements */
 /* Loss head of the full DCN + SPTT training step (the reference has no
  * training): binary cross-entropy on logits z[n],

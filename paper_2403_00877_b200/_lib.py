@@ -111,6 +111,7 @@ _SIGS = {
     "dmt_bce_with_logits": (C.c_int, [vp, vp, i64, i32, f32, vp, vp, vp]),
     "dmt_column_sum_parts": (C.c_int, [vp, i64, i64, vp, vp]),
     "dmt_cross_bwd_pointwise": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, vp]),
+    "dmt_dcn_dx0_term": (C.c_int, [vp, vp, vp, i64, i32, i32, vp]),
     "dmt_sgd_dense": (C.c_int, [vp, vp, i64, f32, i32, vp]),
     "dmt_peer_sum_sgd": (C.c_int, [vp, C.POINTER(C.c_void_p), i32, i64, f32, i32, vp]),
     "dmt_peer_barrier": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), i32, vp, vp]),

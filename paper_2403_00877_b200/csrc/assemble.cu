@@ -242,6 +242,56 @@ __global__ void cross_bwd_pointwise_kernel<double>(const double* __restrict__ g,
   }
 }
 
+// dx0 (+)= g * u: one term of the crossnet's dx0 = sum_l g_{l+1} * u_l, on a
+// side stream beside the (compute-bound) dW GEMMs instead of in the dX GEMM
+// epilogues.  V elements (16 bytes of g / u) per thread and step.
+template <typename T, int V>
+__global__ void dcn_dx0_term_kernel(const T* __restrict__ g, const T* __restrict__ u, float* __restrict__ dx0,
+                                    int64_t n, int accumulate) {
+  const int64_t nv = n / V;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    float gv[V], uv[V], d[V];
+    if constexpr (V == 8) {  // 16-bit types: one 16-byte load per operand
+      const uint4 gr = __ldg(reinterpret_cast<const uint4*>(g + i * 8));
+      const uint4 ur = __ldg(reinterpret_cast<const uint4*>(u + i * 8));
+      const T* gh = reinterpret_cast<const T*>(&gr);
+      const T* uh = reinterpret_cast<const T*>(&ur);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        gv[e] = to_f<T>(gh[e]);
+        uv[e] = to_f<T>(uh[e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        gv[e] = (float)to_d<T>(g[i * V + e]);
+        uv[e] = (float)to_d<T>(u[i * V + e]);
+      }
+    }
+    if (accumulate) {
+#pragma unroll
+      for (int e = 0; e < V; e += 4) {
+        const float4 x = *reinterpret_cast<const float4*>(dx0 + i * V + e);
+        d[e] = x.x; d[e + 1] = x.y; d[e + 2] = x.z; d[e + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) d[e] = 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < V; ++e) d[e] += gv[e] * uv[e];
+#pragma unroll
+    for (int e = 0; e < V; e += 4)
+      *reinterpret_cast<float4*>(dx0 + i * V + e) = make_float4(d[e], d[e + 1], d[e + 2], d[e + 3]);
+  }
+  // tail (n % V elements) by the first threads
+  const int64_t t0 = nv * V + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t0 < n) {
+    const float t = (float)to_d<T>(g[t0]) * (float)to_d<T>(u[t0]);
+    dx0[t0] = accumulate ? dx0[t0] + t : t;
+  }
+}
+
 template <typename T>
 __global__ void sgd_dense_kernel(T* __restrict__ w, const float* __restrict__ g, int64_t n, float lr) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -487,6 +537,24 @@ int dmt_cross_bwd_pointwise(const void* g, const void* x0, const void* u, void* 
     case DMT_F32: dmt::cross_bwd_pointwise_kernel<float><<<grid, 256, 0, s>>>((const float*)g, (const float*)x0, (const float*)u, (float*)gu, dx0, n); break;
     case DMT_BF16: dmt::cross_bwd_pointwise_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)g, (const __nv_bfloat16*)x0, (const __nv_bfloat16*)u, (__nv_bfloat16*)gu, dx0, n); break;
     case DMT_F64: dmt::cross_bwd_pointwise_kernel<double><<<grid, 256, 0, s>>>((const double*)g, (const double*)x0, (const double*)u, (double*)gu, dx0, n); break;
+    default: return DMT_ERR_UNSUPPORTED;
+  }
+  DMT_CHECK_LAUNCH();
+  return DMT_OK;
+}
+
+int dmt_dcn_dx0_term(const void* g, const void* u, float* dx0, int64_t n, int32_t dtype, int32_t accumulate,
+                     dmt_stream_t stream) {
+  if (n == 0) return DMT_OK;
+  if (((uintptr_t)g | (uintptr_t)u | (uintptr_t)dx0) & 15) return DMT_ERR_DOMAIN;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto grid = [&](int V) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(dmt::ceil_div(n / V + 1, 256), DMT_NUM_SMS * 8));
+  };
+  switch (dtype) {
+    case DMT_F32: dmt::dcn_dx0_term_kernel<float, 4><<<grid(4), 256, 0, s>>>((const float*)g, (const float*)u, dx0, n, accumulate); break;
+    case DMT_BF16: dmt::dcn_dx0_term_kernel<__nv_bfloat16, 8><<<grid(8), 256, 0, s>>>((const __nv_bfloat16*)g, (const __nv_bfloat16*)u, dx0, n, accumulate); break;
+    case DMT_F16: dmt::dcn_dx0_term_kernel<__half, 8><<<grid(8), 256, 0, s>>>((const __half*)g, (const __half*)u, dx0, n, accumulate); break;
     default: return DMT_ERR_UNSUPPORTED;
   }
   DMT_CHECK_LAUNCH();

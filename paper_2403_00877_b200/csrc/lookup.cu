@@ -448,7 +448,11 @@ __global__ void bwd_keys_fast_kernel(const dmt_lookup_segment* __restrict__ segs
   }
 }
 
-template <typename T, int VEC, int NV, int CH, int MINB = 2>
+// PF2: the key two positions past each occurrence and the gradient row of the
+// next one are prefetched with the chunk, so a run of length 2 (the common
+// duplicate: ~8 % of unique rows at C2) issues its second gradient row with
+// the head's loads instead of through a dependent key -> value -> row chain.
+template <typename T, int VEC, int NV, int CH, int MINB = 2, bool PF2 = false>
 __global__ void __launch_bounds__(kLookupThreads, MINB)
 bwd_update_fast_kernel(const uint32_t* __restrict__ skeys, const int32_t* __restrict__ svals, int64_t nnz,
                        const char* __restrict__ gbase, const __grid_constant__ ShardTab tab, uint32_t invalid,
@@ -465,6 +469,21 @@ bwd_update_fast_kernel(const uint32_t* __restrict__ skeys, const int32_t* __rest
     s_wp[i] = tab.weights[i];
     s_st[i] = tab.state[i];
   }
+  // shard of a key: a 1024-bucket table over the key space gives the shard of
+  // each bucket's first key, then a short forward walk (usually none) --
+  // instead of a ~log2(shards)-deep chain of dependent shared-memory loads
+  __shared__ uint8_t s_bk[1024];
+  const int bsh = max(0, 32 - __clz(invalid | 1u) - 10);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+    const uint32_t key = (uint32_t)i << bsh;
+    int lo = 0, hi = tab.n - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (s_kb[mid] <= key) lo = mid; else hi = mid - 1;
+    }
+    s_bk[i] = (uint8_t)lo;
+  }
   __syncthreads();
   const int nsh = tab.n;
   const int G = 1 << log2g;
@@ -475,36 +494,34 @@ bwd_update_fast_kernel(const uint32_t* __restrict__ skeys, const int32_t* __rest
   const int64_t stride = (int64_t)gridDim.x * (kLookupThreads / 32) * gpw * CH;
   // software pipeline: the sorted keys / values of the next chunk are loaded
   // while the current chunk's rows are in flight
-  uint32_t nk[CH + 2];
-  int32_t ngv[CH];
+  constexpr int XK = PF2 ? 1 : 0;  // extra keys / values fetched past the chunk
+  uint32_t nk[CH + 2 + XK];
+  int32_t ngv[CH + XK];
   auto fetch = [&](int64_t c0) {
 #pragma unroll
-    for (int u = 0; u <= CH; ++u) nk[u + 1] = (c0 + u < nnz) ? __ldg(skeys + c0 + u) : 0xFFFFFFFEu;
+    for (int u = 0; u <= CH + XK; ++u) nk[u + 1] = (c0 + u < nnz) ? __ldg(skeys + c0 + u) : 0xFFFFFFFEu;
     nk[0] = (c0 > 0 && c0 <= nnz) ? __ldg(skeys + c0 - 1) : 0xFFFFFFFFu;
 #pragma unroll
-    for (int u = 0; u < CH; ++u) ngv[u] = (c0 + u < nnz) ? __ldg(svals + c0 + u) : 0;
+    for (int u = 0; u < CH + XK; ++u) ngv[u] = (c0 + u < nnz) ? __ldg(svals + c0 + u) : 0;
   };
   fetch(warp_global * gpw * CH + (int64_t)gin * CH);
   for (int64_t base = warp_global * gpw * CH; base < nnz; base += stride) {
     const int64_t c0 = base + (int64_t)gin * CH;
-    uint32_t k[CH + 1];
-    int32_t gv[CH];
+    uint32_t k[CH + 1 + XK];
+    int32_t gv[CH + XK];
     const uint32_t prev = nk[0];
 #pragma unroll
-    for (int u = 0; u <= CH; ++u) k[u] = nk[u + 1];
+    for (int u = 0; u <= CH + XK; ++u) k[u] = nk[u + 1];
 #pragma unroll
-    for (int u = 0; u < CH; ++u) gv[u] = ngv[u];
+    for (int u = 0; u < CH + XK; ++u) gv[u] = ngv[u];
     fetch(c0 + stride);
     bool head[CH];
     int sh[CH];
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
       head[u] = (c0 + u < nnz) && k[u] != invalid && k[u] != (u ? k[u - 1] : prev);
-      int lo = 0, hi = nsh - 1;  // last shard with key_base <= key
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (s_kb[mid] <= k[u]) lo = mid; else hi = mid - 1;
-      }
+      int lo = s_bk[min(k[u] >> bsh, 1023u)];  // last shard with key_base <= key
+      while (lo + 1 < nsh && s_kb[lo + 1] <= k[u]) ++lo;
       sh[u] = lo;
     }
     Frag<T, VEC> g0[CH][NV], w[CH][NV];
@@ -521,6 +538,22 @@ bwd_update_fast_kernel(const uint32_t* __restrict__ skeys, const int32_t* __rest
           w[u][v].zero();
         }
       }
+    bool dup2[CH];
+    Frag<T, VEC> g1[PF2 ? CH : 1][NV];
+    if constexpr (PF2) {
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        dup2[u] = head[u] && k[u + 1] == k[u];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int c = (v * G + t) * VEC;
+          if (dup2[u] && c < s_w[sh[u]])
+            g1[u][v].load(reinterpret_cast<const T*>(gbase + ((int64_t)gv[u + 1] << 4)) + c);
+          else
+            g1[u][v].zero();
+        }
+      }
+    }
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
       const int width = s_w[sh[u]];
@@ -530,9 +563,10 @@ bwd_update_fast_kernel(const uint32_t* __restrict__ skeys, const int32_t* __rest
 #pragma unroll
         for (int e = 0; e < VEC; ++e) acc[v][e] = A(0);
         g0[u][v].add_to(acc[v]);
+        if constexpr (PF2) g1[u][v].add_to(acc[v]);
       }
-      if (head[u] && k[u + 1] == k[u]) {
-        for (int64_t j = c0 + u + 1; j < nnz && __ldg(skeys + j) == k[u]; ++j) {
+      if (PF2 ? (dup2[u] && k[u + 2] == k[u]) : (head[u] && k[u + 1] == k[u])) {
+        for (int64_t j = c0 + u + 1 + XK; j < nnz && __ldg(skeys + j) == k[u]; ++j) {
           const T* gp = reinterpret_cast<const T*>(gbase + ((int64_t)__ldg(svals + j) << 4));
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
@@ -1244,16 +1278,17 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
   }
   if (max_b == 0) return DMT_OK;
   // apply variants (DMT_BWD_VARIANT, read once so prepare and apply agree):
-  // 2 (default) register kernel over a CUB radix sort (one occurrence per
-  // group, 4 CTAs / SM); 1 its two-occurrence form; 4 the bulk-copy staged
-  // kernel; 0 the bucketed sort + apply (hand-written bucket scatter, shared-
+  // 7 (default) register kernel over a CUB radix sort, one occurrence per
+  // group, the second row of a duplicate run prefetched (PF2), 2 CTAs / SM;
+  // 5 / 6 the same at 4 / 3 CTAs / SM; 2 without PF2 (4 CTAs / SM); 1 its
+  // two-occurrence form; 4 the bulk-copy staged kernel; 0 the bucketed sort + apply (hand-written bucket scatter, shared-
   // memory bitonic sort per bucket fused with the update) -- all
   // parity-tested.  The bucketed form measured slower at C2 bf16 (apply 0.83
   // vs 0.61 ms; its prepare's bucket-counter atomics 0.19 + 0.14 ms vs the CUB
   // sort), so it is not the default.
   static const int bwd_variant = [] {
     const char* e = getenv("DMT_BWD_VARIANT");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 7;
   }();
   // fast path: no mean pooling, 16-byte aligned gradient rows inside one
   // buffer (offset < 32 GB), <= kMaxShards distinct shards, vector widths
@@ -1408,11 +1443,21 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     if (nv == 1)
       bwd_update_fast_kernel<T, VEC, 1, 4><<<grid_for(log2g), kLookupThreads, 0, s>>>(
           keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
-    else if (nv == 2 && bwd_variant == 1)  // earlier default: 2 occurrences per group, 2 CTAs / SM
+    else if (nv == 2 && bwd_variant == 1)  // two occurrences per group, 2 CTAs / SM
       bwd_update_fast_kernel<T, VEC, 2, 2><<<grid_for(log2g), kLookupThreads, 0, s>>>(
           keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
-    else if (nv == 2)  // 1 occurrence per group, 4 CTAs / SM: measured 0.58 vs 0.69 ms (bf16 C2)
+    else if (nv == 2 && bwd_variant == 2)  // one occurrence per group, 4 CTAs / SM
       bwd_update_fast_kernel<T, VEC, 2, 1, 4><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+    else if (nv == 2 && bwd_variant == 5)
+      bwd_update_fast_kernel<T, VEC, 2, 1, 4, true><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+    else if (nv == 2 && bwd_variant == 6)
+      bwd_update_fast_kernel<T, VEC, 2, 1, 3, true><<<grid_for(log2g), kLookupThreads, 0, s>>>(
+          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+    else if (nv == 2)  // default: PF2, 2 CTAs / SM.  bf16 C2 apply (tools/lookup_bench.py): 580 us
+      // (variant 2, shard binary search) -> 509 (bucketed shard table) -> 505 us (+ PF2)
+      bwd_update_fast_kernel<T, VEC, 2, 1, 2, true><<<grid_for(log2g), kLookupThreads, 0, s>>>(
           keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
     else if (nv <= 4)
       bwd_update_fast_kernel<T, VEC, 4, 1><<<grid_for(log2g), kLookupThreads, 0, s>>>(

@@ -526,6 +526,16 @@ def cross_bwd_pointwise(g, x0, u, gu, dx0) -> None:
             "dmt_cross_bwd_pointwise")
 
 
+def dcn_dx0_term(g: torch.Tensor, u: torch.Tensor, dx0: torch.Tensor, accumulate: bool) -> None:
+    """dx0 (+)= g * u (fp32 dx0; g, u contiguous in the compute dtype)."""
+    if dx0.dtype != torch.float32 or g.shape != u.shape or g.numel() != dx0.numel():
+        raise ShapeError("dcn_dx0_term: g, u of one shape, fp32 dx0 of the same size")
+    if not (g.is_contiguous() and u.is_contiguous() and dx0.is_contiguous()):
+        raise ShapeError("dcn_dx0_term: contiguous operands")
+    L.check(L.lib().dmt_dcn_dx0_term(g.data_ptr(), u.data_ptr(), dx0.data_ptr(), g.numel(), _dt(g), int(accumulate),
+                                     L.stream_ptr()), "dmt_dcn_dx0_term")
+
+
 def sgd_dense(w: torch.Tensor, g: torch.Tensor, lr: float) -> None:
     if g.dtype != torch.float32:
         raise DomainError("dense gradients are fp32")

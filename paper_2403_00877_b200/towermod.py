@@ -152,11 +152,14 @@ def interaction_pairs(num_features: int, num_towers: int, reduction_ratio: float
 # device tower module
 # --------------------------------------------------------------------------- #
 class TowerModule:
-    # DCN backward form: "accumulate" (fp32 dx0 read-modify-written by every
-    # layer's epilogue; the faster one on B200) or "pairs" (no dx0: every g_l
-    # kept, pair-sum final epilogue, bias-gradient column sums fused into the
-    # epilogues; L <= 4) -- both parity-tested
-    dcn_bwd_form = os.environ.get("DMT_DCN_BWD", "accumulate")
+    # DCN backward form (all parity-tested):
+    #   "side" (default): light dX epilogues (x0, g_{l+1} in; g_l, gu_l out),
+    #     dx0 = sum_l g_{l+1} * u_l and the bias-gradient column sums on a side
+    #     stream beside the compute-bound dW GEMMs;
+    #   "accumulate": fp32 dx0 read-modify-written by every layer's epilogue;
+    #   "pairs": no dx0, every g_l kept, pair-sum final epilogue, bias-gradient
+    #     column sums fused into the epilogues (L <= 4).
+    dcn_bwd_form = os.environ.get("DMT_DCN_BWD", "side")
 
     """Device TM of one tower: forward / backward / SGD on libdmt GEMMs.
 
@@ -341,6 +344,8 @@ class TowerModule:
 
         if L_ <= L.GEMM_MAX_PAIRS and self.dcn_bwd_form == "pairs":
             return self._dcn_bwd_pairs(gy, weight_grad)
+        if self.dcn_bwd_form == "side":
+            return self._dcn_bwd_side(gy, weight_grad)
         g = torch.empty((rows, M), dtype=self.dtype, device=dev)
         gu = [torch.empty((rows, M), dtype=self.dtype, device=dev) for _ in range(2)]
         dx0 = torch.empty((rows, M), dtype=f32, device=dev)
@@ -367,6 +372,65 @@ class TowerModule:
                 K.gemm(cur, self.w["w0"], dx, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=g, beta=1.0, aux2=dx0,
                        col_groups=sc[1] if sc else (), col_group_width=sc[0] if sc else 0)
             weight_grad(f"w{layer}", cur, xs[layer])
+        return dx
+
+    def _aux_stream(self) -> torch.cuda.Stream:
+        st = getattr(self, "_aux", None)
+        if st is None or st.device != torch.cuda.current_stream().device:
+            st = self._aux = torch.cuda.Stream(device=torch.cuda.current_stream().device)
+        return st
+
+    def _dcn_bwd_side(self, gy, weight_grad):
+        """Crossnet backward with light dX epilogues (8 bytes / element: x0 and
+        g_{l+1} in, g_l and gu_l out -- the "pairs" form's per-layer GEMMs),
+        while the element-wise rest runs on a side stream beside the next dW
+        GEMM (compute-bound, leaving HBM idle):
+            dx0 = sum_{l=L..1} g_l * u_{l-1}   (dmt_dcn_dx0_term, fp32)
+            db_l = colsum(gu_l),  db_proj = colsum(gy)
+        and the final epilogue is DCN_FINAL: dX = gu_0 W_0 + g_1 + dx0 (with the
+        step-d^-1 column scatter when given).  Same dx0 summation order as the
+        "accumulate" form; g_l enters dx0 as stored (compute dtype)."""
+        xs, us = self._saved
+        x0 = xs[0]
+        rows, M = x0.shape
+        L_ = self.cfg.cross_layers
+        dev, dt = x0.device, self.dtype
+        main, side = torch.cuda.current_stream(), self._aux_stream()
+        G = [None] + [torch.empty((rows, M), dtype=dt, device=dev) for _ in range(L_)]
+        gu = [torch.empty((rows, M), dtype=dt, device=dev) for _ in range(L_)]
+        dx0 = torch.empty((rows, M), dtype=torch.float32, device=dev)
+        bias = {f"b{l}": torch.empty(M, dtype=torch.float32, device=dev) for l in range(L_)}
+        bias["b_proj"] = torch.empty(gy.shape[1], dtype=torch.float32, device=dev)
+
+        def side_work(layer):
+            # g_{layer+1} and gu_layer exist (written by the dX GEMM just issued)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                K.dcn_dx0_term(G[layer + 1], us[layer], dx0, accumulate=layer != L_ - 1)
+                K.column_sum(gu[layer], out=bias[f"b{layer}"])
+                if layer == L_ - 1:
+                    K.column_sum(gy, out=bias["b_proj"])
+
+        K.gemm(gy, self.w["w_proj"], G[L_], trans_b=True, epilogue=L.EPI_DCN_BWD, x0=x0, aux=gu[L_ - 1])
+        side_work(L_ - 1)
+        weight_grad("w_proj", gy, xs[-1])
+        dx = self._new_dx(x0)
+        for layer in range(L_ - 1, -1, -1):
+            cur = gu[layer]
+            if layer > 0:
+                K.gemm(cur, self.w[f"w{layer}"], G[layer], trans_b=True, epilogue=L.EPI_DCN_BWD, c=G[layer + 1],
+                       beta=1.0, x0=x0, aux=gu[layer - 1])
+                side_work(layer - 1)
+                weight_grad(f"w{layer}", cur, xs[layer])
+            else:
+                # the side stream's last dx0 term ran beside dW_1; dW_0 stays
+                # after this GEMM (a fused SGD updates W_0 in place)
+                main.wait_stream(side)
+                sc = self._dx_scatter
+                K.gemm(cur, self.w["w0"], dx, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=G[1], beta=1.0, aux2=dx0,
+                       col_groups=sc[1] if sc else (), col_group_width=sc[0] if sc else 0)
+                weight_grad("w0", cur, xs[0])
+        self.grads.update(bias)
         return dx
 
     def _colsum_part(self, rows, M, dev):

@@ -86,6 +86,115 @@ def test_embedding_backward_is_deterministic():
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
 
 
+_MANY_SHARDS = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2403_00877_b200 import _lib as L
+from paper_2403_00877_b200 import kernels as K
+
+def run(dt, opt):
+    rng = np.random.default_rng(5)
+    dev = torch.device("cuda")
+    # 40 shards of very different sizes (1 .. 3000 rows) in one key space, so
+    # several shard boundaries share a bucket of the apply's shard table
+    sizes = [1, 2, 3, 7, 1, 3000, 5, 1, 1, 64, 900, 2, 2, 2, 17, 1, 1200, 33, 1, 8] * 2
+    width, nbags = 128, 700
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    tables, segs, lens_all, idx_all, g_all = [], [], [], [], []
+    G = torch.empty(len(sizes) * nbags * width, device=dev, dtype=tdt)
+    kb = 0
+    for t, rows in enumerate(sizes):
+        lens = rng.integers(0, 9, size=nbags)
+        idx = (rng.zipf(1.5, size=int(lens.sum())) - 1) % rows
+        W = torch.from_numpy(rng.uniform(-1, 1, (rows, width)).astype(np.float32)).to(dev).to(tdt)
+        g = torch.from_numpy(rng.normal(size=(nbags, width)).astype(np.float32)).to(dev).to(tdt)
+        G[t * nbags * width:(t + 1) * nbags * width] = g.reshape(-1)
+        st = torch.full((rows,), 0.1, dtype=torch.float32, device=dev)
+        segs.append(K.Segment(weights=W, out=G, out_offset=t * nbags * width, out_ld=width, bag_begin=t * nbags,
+                              nbags=nbags, pooling=L.POOL_SUM, key_base=kb, state=st if opt else None))
+        tables.append((W.clone(), st.clone(), W, st, rows))
+        lens_all.append(lens); idx_all.append(idx); g_all.append(g.float().cpu().numpy())
+        kb += rows
+    lens = np.concatenate(lens_all)
+    offs = K.lengths_to_offsets(torch.from_numpy(lens.astype(np.int32)).to(dev))
+    I = torch.from_numpy(np.concatenate(idx_all).astype(np.int32)).to(dev)
+    nnz = int(lens.sum())
+    ws = K.pooled_lookup_bwd_workspace(nnz, kb, len(lens), dev)
+    K.pooled_lookup_bwd(K.SegmentTable(segs, dev), offs, I, nnz, kb,
+                        L.OPT_ROWWISE_ADAGRAD if opt else L.OPT_SGD, 0.05, 1e-8, ws)
+    torch.cuda.synchronize()
+    return tables, lens_all, idx_all, g_all
+
+if __name__ == "__main__":
+    out = {{}}
+    for dt in ("bf16", "fp32"):
+        for opt in (0, 1):
+            tables, *_ = run(dt, opt)
+            for t, (W0, S0, W, S, rows) in enumerate(tables):
+                out[f"{{dt}}_{{opt}}_{{t}}"] = W.float().cpu().numpy()
+                out[f"{{dt}}_{{opt}}_{{t}}_s"] = S.cpu().numpy()
+    np.savez(sys.argv[1], **out)
+"""
+
+
+def _many_shards_module(tmp_path):
+    import importlib.util
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = tmp_path / "many_shards.py"
+    path.write_text(_MANY_SHARDS.format(root=root))
+    spec = importlib.util.spec_from_file_location("many_shards", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod, path
+
+
+@pytest.mark.parametrize("opt", [0, 1])
+@pytest.mark.parametrize("dt", ["bf16", "fp32"])
+def test_embedding_backward_many_shards(dt, opt, tmp_path):
+    """40 shards of 1..3000 rows in one key space: the apply's shard table
+    (bucket of the key -> shard of its first key, then a forward walk) must
+    resolve every key to its own shard."""
+    mod, _ = _many_shards_module(tmp_path)
+    tables, lens_all, idx_all, g_all = mod.run(dt, opt)
+    # fp32: the 1-row shards sum ~2,800 N(0, 1) gradient rows in fp32 (the
+    # oracle in fp64): 2e-5 absolute after lr 0.05, hence atol 5e-5
+    rtol, atol = (1e-2, 1e-2) if dt == "bf16" else (1e-5, 5e-5)
+    for (W0, S0, W, S, rows), lens, idx, g in zip(tables, lens_all, idx_all, g_all):
+        table = W0.float().cpu().numpy().astype(np.float64)
+        uniq, grads = oracle.embedding_row_grads(rows, lens, idx, g.astype(np.float64), "sum")
+        if opt:
+            want, want_s = oracle.apply_rowwise_adagrad(table, S0.double().cpu().numpy(), uniq, grads, 0.05, 1e-8)
+            np.testing.assert_allclose(S.double().cpu().numpy(), want_s, rtol=1e-5, atol=1e-6)
+        else:
+            want = oracle.apply_sgd(table, uniq, grads, 0.05)
+        np.testing.assert_allclose(W.double().cpu().numpy(), want, rtol=rtol, atol=atol)
+
+
+def test_embedding_backward_apply_variants_agree(tmp_path):
+    """Every apply variant (DMT_BWD_VARIANT; read once per process, so one
+    subprocess each) sums a run's rows in the same order: bit-identical
+    tables and optimizer state."""
+    import os
+    import subprocess
+    import sys
+
+    _, path = _many_shards_module(tmp_path)
+    res = {}
+    for v in (7, 0, 1, 2, 4, 5, 6):
+        out = tmp_path / f"v{v}.npz"
+        env = dict(os.environ, DMT_BWD_VARIANT=str(v))
+        subprocess.run([sys.executable, str(path), str(out)], env=env, check=True, timeout=600)
+        res[v] = np.load(out)
+    for v, r in res.items():
+        for k in r.files:
+            if k.split("_")[1] == "0":  # SGD: identical summation order -> identical bits
+                assert np.array_equal(r[k], res[7][k]), (v, k)
+            else:  # row-wise Adagrad: the squared-norm reduction tree differs between kernels
+                np.testing.assert_allclose(r[k], res[7][k], rtol=2e-6, atol=1e-7, err_msg=f"{v} {k}")
+
+
 def _tm_objects(kind, F, N, dt, seed=0, layers=3):
     import paper_2403_00877_b200 as P
 
@@ -105,10 +214,11 @@ def _tm_objects(kind, F, N, dt, seed=0, layers=3):
 # DCN variants: 3 layers / width 192 = pair-sum final epilogue + fused bias
 # column sums; width 48 = pair sum on the unaligned epilogue path with separate
 # column sums; 5 layers = the fp32 dx0-accumulator form (more than 4 pairs).
+# "side" (the default) computes dx0 and the bias gradients on a side stream.
 @pytest.mark.parametrize("kind,F,N,layers", [("dlrm", 6, 32, 3), ("dcn", 6, 32, 3), ("dcn", 3, 16, 3),
                                              ("dcn", 6, 32, 5), ("dcn", 4, 32, 1)])
 @pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
-@pytest.mark.parametrize("form", ["accumulate", "pairs"])
+@pytest.mark.parametrize("form", ["side", "accumulate", "pairs"])
 def test_tower_module_backward_vs_oracle(kind, F, N, layers, dt, form, monkeypatch):
     import paper_2403_00877_b200 as P
 
