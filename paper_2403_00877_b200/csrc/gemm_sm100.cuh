@@ -1405,6 +1405,8 @@ static int dispatch_n(const dmt_gemm_args* a, const void* alo, const void* blo, 
       const bool pair = pair_ok && !(a->flags & DMT_GEMM_SINGLE_CTA) &&
                         ((a->flags & DMT_GEMM_CLUSTER) || (bn == 256 && a->n >= 2048));
       if (pair) {
+        // (6 stages fit too -- 231,680 B -- and measured no faster: the pair
+        // mainloop is bound by L2 throughput, not by stage depth)
         if (bn == 256) return launch<256, 1, 0, 5, TIN, TO, AMN, BMN, FEAT, 2>(a, alo, blo, s);
         if constexpr (!BMN) return launch<192, 1, 0, 6, TIN, TO, AMN, BMN, FEAT, 2>(a, alo, blo, s);
       }

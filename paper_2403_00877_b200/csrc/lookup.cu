@@ -12,6 +12,7 @@
 // destination layout, which is how the step-c permute and step-d stacking are
 // fused into the lookup epilogue (zero extra bytes).
 #include <cstdlib>
+#include <string>
 
 #include <cub/cub.cuh>
 
@@ -1213,10 +1214,228 @@ bwd_bucket_apply_kernel(const uint64_t* __restrict__ items, const uint32_t* __re
   }
 }
 
+// ---- hand-written LSD radix sort of (key, value) pairs -----------------------
+// The prepare's sort: keys < 2^end_bit (25 bits at C2: 26 shards x 1M rows),
+// values = 16-byte gradient-row offsets.  ceil(end_bit / 9) stable passes of
+// <= 9-bit digits (3 at C2, vs CUB onesweep's 4 x 8 bits), each pass three
+// kernels over 4096-element tiles:
+//   upsweep   per-tile digit histogram (shared-memory atomics) -> counts[d][t]
+//   scan      exclusive scan of counts in digit-major order (tile order within
+//             a digit: what makes the pass stable across tiles)
+//   downsweep stable rank inside the tile -- warp w ranks its 512-element
+//             sub-tile as 4 independent 128-element streams (4 steps of 32,
+//             __match_any_sync against a per-stream digit counter; the four
+//             chains interleave), streams and warps combined in element
+//             order -- then the tile is reordered by (digit, rank) in shared
+//             memory and stored so consecutive threads write consecutive
+//             slots of one digit's run.
+// The order equals any stable sort's (identical to the CUB path), so the
+// apply's summation order and results are unchanged.
+constexpr int kRadixBits = 9;
+constexpr int kRadixBins = 1 << kRadixBits;
+constexpr int kRadixThreads = 256;
+constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kRadixItems = 16;                              // per thread
+constexpr int kRadixTile = kRadixThreads * kRadixItems;      // 4096
+constexpr int kRadixSub = kRadixTile / kRadixWarps;          // 512 per warp
+
+inline int radix_passes(int end_bit) { return (end_bit + kRadixBits - 1) / kRadixBits; }
+inline int radix_digit_bits(int end_bit) {
+  const int np = radix_passes(end_bit);
+  return (end_bit + np - 1) / np;
+}
+
+__global__ void __launch_bounds__(kRadixThreads) radix_upsweep(const uint32_t* __restrict__ keys, int64_t n,
+                                                               int shift, uint32_t mask, int64_t ntiles,
+                                                               uint32_t* __restrict__ counts) {
+  __shared__ uint32_t hist[kRadixBins];
+  for (int i = threadIdx.x; i < kRadixBins; i += kRadixThreads) hist[i] = 0;
+  __syncthreads();
+  const int64_t t = blockIdx.x;
+  const int64_t base = t * kRadixTile;
+  uint32_t k[kRadixItems];
+#pragma unroll
+  for (int i = 0; i < kRadixItems; ++i) {
+    const int64_t idx = base + i * kRadixThreads + threadIdx.x;
+    k[i] = idx < n ? __ldg(keys + idx) : 0xFFFFFFFFu;
+  }
+#pragma unroll
+  for (int i = 0; i < kRadixItems; ++i)
+    if (k[i] != 0xFFFFFFFFu) atomicAdd(&hist[(k[i] >> shift) & mask], 1u);
+  __syncthreads();
+  for (int d = threadIdx.x; d <= (int)mask; d += kRadixThreads) counts[(int64_t)d * ntiles + t] = hist[d];
+}
+
+constexpr int kRadixStreams = 4;                                  // independent rank chains per warp
+constexpr int kRadixStreamLen = kRadixSub / kRadixStreams;        // 128 elements each
+
+__global__ void __launch_bounds__(kRadixThreads, 3) radix_downsweep(
+    const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+    int32_t* __restrict__ vals_out, int64_t n, int shift, int dbits, int64_t ntiles,
+    const uint32_t* __restrict__ offsets) {
+  extern __shared__ __align__(16) uint8_t radix_smem[];
+  // [warp * streams + stream][digit] counts -> exclusive prefix in element order
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(radix_smem);
+  uint32_t* skeys = reinterpret_cast<uint32_t*>(wcnt + kRadixWarps * kRadixStreams * kRadixBins);
+  int32_t* svals = reinterpret_cast<int32_t*>(skeys + kRadixTile);
+  uint32_t* dstart = reinterpret_cast<uint32_t*>(svals + kRadixTile);  // tile-local start of each digit
+  uint32_t* goff = dstart + kRadixBins;                                 // global start of (digit, tile)
+  uint32_t* wsum = goff + kRadixBins;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t mask = (1u << dbits) - 1u;
+  const int64_t t = blockIdx.x;
+  const int64_t base = t * kRadixTile;
+  const int64_t wbase = base + warp * kRadixSub;
+  {
+    uint4* z = reinterpret_cast<uint4*>(wcnt);
+    constexpr int nz = kRadixWarps * kRadixStreams * kRadixBins * 2 / 16;
+    for (int i = threadIdx.x; i < nz; i += kRadixThreads) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  for (int d = threadIdx.x; d < kRadixBins; d += kRadixThreads)
+    goff[d] = d <= (int)mask ? offsets[(int64_t)d * ntiles + t] : 0u;
+  // item i = stream (i % S), step (i / S): element wbase + stream * 128 + step * 32 + lane
+  uint32_t k[kRadixItems];
+  int32_t v[kRadixItems];
+#pragma unroll
+  for (int i = 0; i < kRadixItems; ++i) {
+    const int64_t idx = wbase + (i % kRadixStreams) * kRadixStreamLen + (i / kRadixStreams) * 32 + lane;
+    const bool ok = idx < n;
+    k[i] = ok ? __ldg(keys_in + idx) : 0xFFFFFFFFu;
+    v[i] = ok ? __ldg(vals_in + idx) : 0;
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+  uint16_t r[kRadixItems];
+  uint16_t* myc = wcnt + warp * kRadixStreams * kRadixBins;
+#pragma unroll
+  for (int step = 0; step < kRadixItems / kRadixStreams; ++step) {
+    uint32_t d[kRadixStreams], m[kRadixStreams], before[kRadixStreams];
+    bool ok[kRadixStreams];
+#pragma unroll
+    for (int q = 0; q < kRadixStreams; ++q) {  // S independent chains: their latencies overlap
+      const int i = step * kRadixStreams + q;
+      ok[q] = k[i] != 0xFFFFFFFFu;
+      d[q] = ok[q] ? (k[i] >> shift) & mask : (uint32_t)kRadixBins - 1u;
+      m[q] = __match_any_sync(0xffffffffu, d[q]) & __ballot_sync(0xffffffffu, ok[q]);
+      before[q] = myc[q * kRadixBins + d[q]];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < kRadixStreams; ++q) {
+      const int i = step * kRadixStreams + q;
+      if (ok[q]) {
+        r[i] = (uint16_t)(before[q] + __popc(m[q] & lt));
+        if ((m[q] & lt) == 0) myc[q * kRadixBins + d[q]] = (uint16_t)(before[q] + __popc(m[q]));
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive prefix over (warp, stream) -- element order
+  for (int d = threadIdx.x; d < kRadixBins; d += kRadixThreads) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kRadixWarps * kRadixStreams; ++w) {
+      const uint32_t c = wcnt[w * kRadixBins + d];
+      wcnt[w * kRadixBins + d] = (uint16_t)run;
+      run += c;
+    }
+    dstart[d] = run;  // tile histogram for now
+  }
+  __syncthreads();
+  {  // exclusive scan of the tile histogram over digits (2 digits per thread)
+    const int d0 = threadIdx.x * 2;
+    const uint32_t a = dstart[d0], b = dstart[d0 + 1];
+    uint32_t x = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int w = 0; w < kRadixWarps; ++w)
+      if (w < warp) wpre += wsum[w];
+    const uint32_t excl = wpre + x - (a + b);
+    __syncthreads();
+    dstart[d0] = excl;
+    dstart[d0 + 1] = excl + a;
+  }
+  __syncthreads();
+  // reorder the tile by (digit, rank) in shared memory ...
+#pragma unroll
+  for (int i = 0; i < kRadixItems; ++i) {
+    if (k[i] == 0xFFFFFFFFu) continue;
+    const uint32_t d = (k[i] >> shift) & mask;
+    const uint32_t pos = dstart[d] + myc[(i % kRadixStreams) * kRadixBins + d] + r[i];
+    skeys[pos] = k[i];
+    svals[pos] = v[i];
+  }
+  __syncthreads();
+  // ... and store it so consecutive threads write consecutive slots of a run
+  const int cnt = n - base < kRadixTile ? (int)(n - base) : kRadixTile;
+  for (int i = threadIdx.x; i < cnt; i += kRadixThreads) {
+    const uint32_t kk = skeys[i];
+    const uint32_t d = (kk >> shift) & mask;
+    const int64_t dst = (int64_t)goff[d] + (i - (int64_t)dstart[d]);
+    keys_out[dst] = kk;
+    vals_out[dst] = svals[i];
+  }
+}
+
+constexpr size_t kRadixDownSmem = (size_t)kRadixWarps * kRadixStreams * kRadixBins * 2 + (size_t)kRadixTile * 8 +
+                                  (size_t)kRadixBins * 8 + kRadixWarps * 4;
+
+inline int64_t radix_tiles(int64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
+
+inline size_t radix_scan_bytes(int64_t n) {
+  size_t bytes = 0;
+  const int64_t items = radix_tiles(std::max<int64_t>(n, 1)) * kRadixBins;
+  cub::DeviceScan::ExclusiveSum((void*)nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)items);
+  return bytes;
+}
+
+// Sorts n pairs by the low end_bit bits of the keys; the result lands in the
+// `_out` buffers when radix_passes(end_bit) is odd, else back in `_in`.
+inline int radix_sort_pairs(uint32_t* keys_in, int32_t* vals_in, uint32_t* keys_out, int32_t* vals_out, int64_t n,
+                            int end_bit, uint32_t* counts, uint32_t* offsets, void* scan_tmp, size_t scan_bytes,
+                            cudaStream_t s) {
+  if (n <= 0) return DMT_OK;
+  if (n >= (int64_t(1) << 31)) return DMT_ERR_UNSUPPORTED;
+  const int np = radix_passes(end_bit), db = radix_digit_bits(end_bit);
+  const uint32_t mask = (1u << db) - 1u;
+  const int64_t nt = radix_tiles(n);
+  const int items = (int)(nt * (mask + 1));
+  uint32_t *ki = keys_in, *ko = keys_out;
+  int32_t *vi = vals_in, *vo = vals_out;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(radix_downsweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRadixDownSmem) !=
+        cudaSuccess)
+      return DMT_ERR_CUDA;
+    attr = true;
+  }
+  for (int pass = 0; pass < np; ++pass) {
+    const int shift = pass * db;
+    radix_upsweep<<<(unsigned)nt, kRadixThreads, 0, s>>>(ki, n, shift, mask, nt, counts);
+    DMT_CHECK_LAUNCH();
+    size_t sb = scan_bytes;
+    if (cub::DeviceScan::ExclusiveSum(scan_tmp, sb, counts, offsets, items, s) != cudaSuccess) return DMT_ERR_CUDA;
+    radix_downsweep<<<(unsigned)nt, kRadixThreads, kRadixDownSmem, s>>>(ki, vi, ko, vo, n, shift, db, nt, offsets);
+    DMT_CHECK_LAUNCH();
+    std::swap(ki, ko);
+    std::swap(vi, vo);
+  }
+  return DMT_OK;
+}
+
 struct BwdLayout {
   size_t keys_in, keys_out, vals_in, vals_out, recs, cub_temp, total;
   size_t cub_bytes;
   size_t bcounts, boffs, bcursor, items, scratch;  // bucketed path
+  size_t rcounts, roffs, rscan, rscan_bytes;      // radix path
   int bshift;
   int64_t nbuckets;
 };
@@ -1253,6 +1472,11 @@ inline BwdLayout bwd_layout(int64_t nnz, int64_t key_space, int64_t nbags) {
   L.bcursor = off; off = align256(off + nbk * 4);
   L.items = off; off = align256(off + n * 8);
   L.scratch = off; off = align256(off + 2 * n * 8 + (size_t)kBktCap * 8);
+  const size_t ritems = (size_t)radix_tiles((int64_t)n) * kRadixBins;
+  L.rcounts = off; off = align256(off + ritems * 4);
+  L.roffs = off; off = align256(off + ritems * 4);
+  L.rscan_bytes = radix_scan_bytes((int64_t)n);
+  L.rscan = off; off = align256(off + L.rscan_bytes);
   L.total = off;
   return L;
 }
@@ -1342,6 +1566,17 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
   BagRec* recs = (BagRec*)(w + L.recs);
   const uint32_t invalid = (uint32_t)key_space;
 
+  // sort of the prepare (DMT_BWD_SORT): 0 (default) the hand-written radix
+  // sort above (3 passes of 9 / 8 / 8 bits at C2), 1 CUB onesweep (4 passes)
+  static const int bwd_sort = [] {
+    const char* e = getenv("DMT_BWD_SORT");
+    return e && std::string(e) == "cub" ? 1 : 0;
+  }();
+  const int end_bit = end_bit_for((uint64_t)key_space);
+  // where the sorted pairs land: CUB and odd radix pass counts -> `_out`
+  const bool sorted_in_out = bwd_sort == 1 || (radix_passes(end_bit) & 1);
+  const uint32_t* skeys = sorted_in_out ? keys_out : keys_in;
+  const int32_t* svals = sorted_in_out ? vals_out : vals_in;
   const bool bucketed = fast && bwd_variant == 0;
   uint32_t* bcounts = (uint32_t*)(w + L.bcounts);
   uint32_t* boffs = (uint32_t*)(w + L.boffs);
@@ -1372,10 +1607,16 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     else
       bwd_keys_kernel<<<kg, 256, 0, s>>>(segs, offsets, indices, invalid, keys_in, vals_in, recs, (int)sizeof(T));
     DMT_CHECK_LAUNCH();
-    size_t cub_bytes = L.cub_bytes;
-    if (cub::DeviceRadixSort::SortPairs((void*)(w + L.cub_temp), cub_bytes, keys_in, keys_out, vals_in, vals_out,
-                                        (int)nnz, 0, end_bit_for((uint64_t)key_space), s) != cudaSuccess)
-      return DMT_ERR_CUDA;
+    if (bwd_sort == 1) {
+      size_t cub_bytes = L.cub_bytes;
+      if (cub::DeviceRadixSort::SortPairs((void*)(w + L.cub_temp), cub_bytes, keys_in, keys_out, vals_in, vals_out,
+                                          (int)nnz, 0, end_bit, s) != cudaSuccess)
+        return DMT_ERR_CUDA;
+    } else {
+      const int rc = radix_sort_pairs(keys_in, vals_in, keys_out, vals_out, nnz, end_bit, (uint32_t*)(w + L.rcounts),
+                                      (uint32_t*)(w + L.roffs), (void*)(w + L.rscan), L.rscan_bytes, s);
+      if (rc != DMT_OK) return rc;
+    }
   }
   if (!(phase & 2)) return DMT_OK;
   constexpr int VEC = Vec16<T>::N;
@@ -1423,11 +1664,11 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     if (uniform_w) {
       int rc;
       if (nvec_all == 8)
-        rc = launch_async_update<T, 8>(keys_out, vals_out, nnz, gbase, tab, invalid, opt, lr, eps, s);
+        rc = launch_async_update<T, 8>(skeys, svals, nnz, gbase, tab, invalid, opt, lr, eps, s);
       else if (nvec_all == 16)
-        rc = launch_async_update<T, 16>(keys_out, vals_out, nnz, gbase, tab, invalid, opt, lr, eps, s);
+        rc = launch_async_update<T, 16>(skeys, svals, nnz, gbase, tab, invalid, opt, lr, eps, s);
       else
-        rc = launch_async_update<T, 32>(keys_out, vals_out, nnz, gbase, tab, invalid, opt, lr, eps, s);
+        rc = launch_async_update<T, 32>(skeys, svals, nnz, gbase, tab, invalid, opt, lr, eps, s);
       if (rc != DMT_OK) return rc;
       DMT_CHECK_LAUNCH();
       return DMT_OK;
@@ -1442,26 +1683,26 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     const int nv = (nvec + G - 1) / G;
     if (nv == 1)
       bwd_update_fast_kernel<T, VEC, 1, 4><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
     else if (nv == 2 && bwd_variant == 1)  // two occurrences per group, 2 CTAs / SM
       bwd_update_fast_kernel<T, VEC, 2, 2><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
     else if (nv == 2 && bwd_variant == 2)  // one occurrence per group, 4 CTAs / SM
       bwd_update_fast_kernel<T, VEC, 2, 1, 4><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
     else if (nv == 2 && bwd_variant == 5)
       bwd_update_fast_kernel<T, VEC, 2, 1, 4, true><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
     else if (nv == 2 && bwd_variant == 6)
       bwd_update_fast_kernel<T, VEC, 2, 1, 3, true><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
     else if (nv == 2)  // default: PF2, 2 CTAs / SM.  bf16 C2 apply (tools/lookup_bench.py): 580 us
       // (variant 2, shard binary search) -> 509 (bucketed shard table) -> 505 us (+ PF2)
       bwd_update_fast_kernel<T, VEC, 2, 1, 2, true><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
     else if (nv <= 4)
       bwd_update_fast_kernel<T, VEC, 4, 1><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, gbase, tab, invalid, log2g, opt, lr, eps);
     else
       return DMT_ERR_UNSUPPORTED;
   } else if (vec_ok) {
@@ -1471,13 +1712,13 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     const int nv = (nvec + G - 1) / G;
     if (nv == 1)
       bwd_update_kernel<T, VEC, 1, 4><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, recs, invalid, log2g, opt, lr, eps);
     else if (nv == 2)
       bwd_update_kernel<T, VEC, 2, 2><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, recs, invalid, log2g, opt, lr, eps);
     else if (nv <= 4)
       bwd_update_kernel<T, VEC, 4, 1><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, recs, invalid, log2g, opt, lr, eps);
     else
       return DMT_ERR_UNSUPPORTED;
   } else {
@@ -1487,13 +1728,13 @@ int launch_bwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     const int nv = (max_w + G - 1) / G;
     if (nv == 1)
       bwd_update_kernel<T, 1, 1, 4><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, recs, invalid, log2g, opt, lr, eps);
     else if (nv <= 4)
       bwd_update_kernel<T, 1, 4, 1><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, recs, invalid, log2g, opt, lr, eps);
     else
       bwd_update_kernel<T, 1, 8, 1><<<grid_for(log2g), kLookupThreads, 0, s>>>(
-          keys_out, vals_out, nnz, recs, invalid, log2g, opt, lr, eps);
+          skeys, svals, nnz, recs, invalid, log2g, opt, lr, eps);
   }
   DMT_CHECK_LAUNCH();
   return DMT_OK;

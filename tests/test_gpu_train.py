@@ -92,12 +92,15 @@ sys.path.insert(0, {root!r})
 from paper_2403_00877_b200 import _lib as L
 from paper_2403_00877_b200 import kernels as K
 
-def run(dt, opt):
+def run(dt, opt, big=False):
     rng = np.random.default_rng(5)
     dev = torch.device("cuda")
     # 40 shards of very different sizes (1 .. 3000 rows) in one key space, so
-    # several shard boundaries share a bucket of the apply's shard table
+    # several shard boundaries share a bucket of the apply's shard table;
+    # 14-bit keys = 2 radix passes, big (a 300k-row shard added) 19 bits = 3
     sizes = [1, 2, 3, 7, 1, 3000, 5, 1, 1, 64, 900, 2, 2, 2, 17, 1, 1200, 33, 1, 8] * 2
+    if big:
+        sizes[7] = 300000
     width, nbags = 128, 700
     tdt = torch.bfloat16 if dt == "bf16" else torch.float32
     tables, segs, lens_all, idx_all, g_all = [], [], [], [], []
@@ -129,10 +132,11 @@ if __name__ == "__main__":
     out = {{}}
     for dt in ("bf16", "fp32"):
         for opt in (0, 1):
-            tables, *_ = run(dt, opt)
-            for t, (W0, S0, W, S, rows) in enumerate(tables):
-                out[f"{{dt}}_{{opt}}_{{t}}"] = W.float().cpu().numpy()
-                out[f"{{dt}}_{{opt}}_{{t}}_s"] = S.cpu().numpy()
+            for big in (0, 1):
+                tables, *_ = run(dt, opt, bool(big))
+                for t, (W0, S0, W, S, rows) in enumerate(tables):
+                    out[f"{{dt}}_{{opt}}_{{big}}_{{t}}"] = W.float().cpu().numpy()
+                    out[f"{{dt}}_{{opt}}_{{big}}_{{t}}_s"] = S.cpu().numpy()
     np.savez(sys.argv[1], **out)
 """
 
@@ -150,14 +154,15 @@ def _many_shards_module(tmp_path):
     return mod, path
 
 
+@pytest.mark.parametrize("big", [False, True])
 @pytest.mark.parametrize("opt", [0, 1])
 @pytest.mark.parametrize("dt", ["bf16", "fp32"])
-def test_embedding_backward_many_shards(dt, opt, tmp_path):
+def test_embedding_backward_many_shards(dt, opt, big, tmp_path):
     """40 shards of 1..3000 rows in one key space: the apply's shard table
     (bucket of the key -> shard of its first key, then a forward walk) must
     resolve every key to its own shard."""
     mod, _ = _many_shards_module(tmp_path)
-    tables, lens_all, idx_all, g_all = mod.run(dt, opt)
+    tables, lens_all, idx_all, g_all = mod.run(dt, opt, big)
     # fp32: the 1-row shards sum ~2,800 N(0, 1) gradient rows in fp32 (the
     # oracle in fp64): 2e-5 absolute after lr 0.05, hence atol 5e-5
     rtol, atol = (1e-2, 1e-2) if dt == "bf16" else (1e-5, 5e-5)
@@ -173,26 +178,31 @@ def test_embedding_backward_many_shards(dt, opt, tmp_path):
 
 
 def test_embedding_backward_apply_variants_agree(tmp_path):
-    """Every apply variant (DMT_BWD_VARIANT; read once per process, so one
-    subprocess each) sums a run's rows in the same order: bit-identical
-    tables and optimizer state."""
+    """Every apply variant (DMT_BWD_VARIANT) and both sorts (DMT_BWD_SORT: the
+    hand-written radix sort, CUB) -- read once per process, so one subprocess
+    each -- sum a run's rows in the same order: bit-identical tables and
+    optimizer state."""
     import os
     import subprocess
     import sys
 
     _, path = _many_shards_module(tmp_path)
     res = {}
-    for v in (7, 0, 1, 2, 4, 5, 6):
+    for v in ("7", "cub", "0", "1", "2", "4", "5", "6"):
         out = tmp_path / f"v{v}.npz"
-        env = dict(os.environ, DMT_BWD_VARIANT=str(v))
+        env = dict(os.environ)
+        if v == "cub":
+            env["DMT_BWD_SORT"] = "cub"
+        else:
+            env["DMT_BWD_VARIANT"] = v
         subprocess.run([sys.executable, str(path), str(out)], env=env, check=True, timeout=600)
         res[v] = np.load(out)
     for v, r in res.items():
         for k in r.files:
-            if k.split("_")[1] == "0":  # SGD: identical summation order -> identical bits
-                assert np.array_equal(r[k], res[7][k]), (v, k)
+            if k.split("_")[1] == "0" or v == "cub":  # same summation order -> identical bits
+                assert np.array_equal(r[k], res["7"][k]), (v, k)
             else:  # row-wise Adagrad: the squared-norm reduction tree differs between kernels
-                np.testing.assert_allclose(r[k], res[7][k], rtol=2e-6, atol=1e-7, err_msg=f"{v} {k}")
+                np.testing.assert_allclose(r[k], res["7"][k], rtol=2e-6, atol=1e-7, err_msg=f"{v} {k}")
 
 
 def _tm_objects(kind, F, N, dt, seed=0, layers=3):
