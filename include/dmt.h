@@ -275,7 +275,10 @@ enum dmt_gemm_flags {
   DMT_GEMM_CLUSTER = 32,
   DMT_GEMM_SINGLE_CTA = 64,
   DMT_GEMM_BN_SHIFT = 8,
-  DMT_GEMM_BN_MASK = 0xF00
+  DMT_GEMM_BN_MASK = 0xF00,
+  /* tuning override: keep the output stores of the register-direct epilogue
+   * per-thread instead of TMA bulk stores */
+  DMT_GEMM_NO_TMA_STORE = 0x1000
 };
 
 typedef struct dmt_gemm_args {

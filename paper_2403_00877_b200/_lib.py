@@ -22,6 +22,7 @@ EPI_NONE, EPI_BIAS, EPI_CROSS, EPI_ACC, EPI_DCN_BWD, EPI_DCN_FINAL = 0, 1, 2, 3,
 EPI_BIAS_RELU, EPI_RELU_BWD = 6, 7
 GEMM_TRANS_A, GEMM_TRANS_B, GEMM_AUX2_ACCUM, GEMM_SCALE_ACC = 1, 2, 4, 8
 GEMM_NO_PREFETCH, GEMM_BN_SHIFT, GEMM_CLUSTER, GEMM_SINGLE_CTA = 16, 8, 32, 64  # tuning overrides
+GEMM_NO_TMA_STORE = 0x1000
 GEMM_MAX_PAIRS = 4
 GEMM_MAX_OUT_GROUPS = 8
 GEMM_MAX_COL_GROUPS = 32

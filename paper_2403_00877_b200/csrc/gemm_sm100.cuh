@@ -28,6 +28,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <type_traits>
 
 #include "common.cuh"
@@ -313,6 +314,10 @@ struct Params {
   int64_t colg_ld[DMT_GEMM_MAX_COL_GROUPS];
   int ksplit;     // split-K: units = tiles x ksplit; split s covers K blocks [s*kbs, (s+1)*kbs)
   int kbs;        //   and writes its raw fp32 accumulator at output rows + s * m (workspace)
+  int tma_out;    // direct path: bit 0 = output stored by TMA (emaps.od)
+  int direct;     // register-direct epilogue (no shared-memory staging); DMT_GEMM_EPI=staged turns it off
+  int dbg;        // experiment only (DMT_GEMM_DBG): 1 skip epilogue work, 2 / 16 direct epilogue without
+                  // stores / TMEM loads, 4 skip MMAs, 8 skip TMA loads
 };
 
 // Output row address.  The grouped layout (per-feature DLRM projection rows
@@ -522,9 +527,13 @@ __device__ __forceinline__ float stored(float x) {
   return to_f<T>(from_f<T>(x));
 }
 
+// av: when non-null, the aux output (CROSS u / DCN_BWD gu) goes there instead
+// of global memory; store_out = false leaves the output in v (TMA-stored
+// epilogue path).
 template <typename TIN, typename TO, bool FEAT>
 __device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t col, float* v,
-                                           const EpiIn<TIN, TO>& in, float* gs, int64_t soff) {
+                                           const EpiIn<TIN, TO>& in, float* gs, int64_t soff,
+                                           float* av = nullptr, bool store_out = true) {
   const int e = p.epilogue;
   if (e == DMT_EPI_BIAS || e == DMT_EPI_CROSS || e == DMT_EPI_BIAS_RELU) {
     float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + col));
@@ -547,7 +556,12 @@ __device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t
     float a[8], b[8];
     rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.x0, a);
     rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.u, b);
-    if (p.aux) store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, v);
+    if (av) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) av[j] = v[j];
+    } else if (p.aux) {
+      store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, v);
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = a[j] * v[j] + b[j];
   } else if (e == DMT_EPI_ACC || e == DMT_EPI_DCN_BWD || e == DMT_EPI_DCN_FINAL) {
@@ -571,7 +585,12 @@ __device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t
       rawcvt<typename EpiIn<TIN, TO>::RI, TIN>(in.x0, x0);
 #pragma unroll
       for (int j = 0; j < 8; ++j) x0[j] *= v[j];
-      store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, x0);
+      if (av) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) av[j] = x0[j];
+      } else {
+        store8<TIN>(reinterpret_cast<TIN*>(p.aux) + xo, x0);
+      }
       if (gs) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) gs[j] = stored<TIN>(x0[j]);
@@ -590,7 +609,46 @@ __device__ __forceinline__ void epi_finish(const Params& p, int64_t row, int64_t
       }
     }
   }
-  store8<TO>(out_ptr<TO>(p, row + soff, col), v);  // soff: split-K workspace rows
+  if (store_out) store8<TO>(out_ptr<TO>(p, row + soff, col), v);  // soff: split-K workspace rows
+}
+
+// ---- TMA-stored epilogue (register-direct path) ----------------------------
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(smem))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// One row (this lane's) of a 32 x 32 output chunk into an unswizzled staging
+// tile (row pitch 32 * sizeof(T)) for a TMA store.  Store j of lane r writes
+// 16-byte piece (j + s_r) mod P, s_r chosen so that every 8-lane phase covers
+// all 32 banks (bf16: rows 64 B apart -> s = r / 2; fp32: 128 B -> s = r).
+template <typename T>
+__device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float* v) {
+  constexpr int P = 32 * (int)sizeof(T) / 16;  // 16-byte pieces per row
+  uint4 ch[P];
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    constexpr int E = 16 / (int)sizeof(T);
+    T* h = reinterpret_cast<T*>(&ch[c]);
+#pragma unroll
+    for (int e = 0; e < E; ++e) h[e] = from_f<T>(v[c * E + e]);
+  }
+  const int sft = sizeof(T) == 4 ? lane : (lane >> 1);
+  uint4* row = reinterpret_cast<uint4*>(buf + lane * 32 * (int)sizeof(T));
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const int idx = (j + sft) & (P - 1);
+    uint4 x = ch[0];
+#pragma unroll
+    for (int c = 1; c < P; ++c)
+      if (idx == c) x = ch[c];
+    row[idx] = x;
+  }
 }
 
 // The epilogue operands of a tile (x0 / xl / C / dx0 blocks) do not depend on
@@ -607,6 +665,7 @@ __device__ __forceinline__ void l2_prefetch_2d(const CUtensorMap* map, int c0, i
 
 struct EpiMaps {
   CUtensorMap x0, xl, c, d2;
+  CUtensorMap od;  // TMA store of the output (32 x 32 boxes)
 };
 
 constexpr int kStileFloats = 32 * 33;
@@ -731,7 +790,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          if constexpr (CL == 2) {
+          if (p.dbg & 8) {  // experiment: no operand loads (MMA-only rate)
+            if (crank == 0) mbar_arrive(&full[stage]);
+          } else if constexpr (CL == 2) {
             // both CTAs' loads complete on the leader's barrier; the leader
             // expects the pair's bytes
             if (crank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
@@ -743,7 +804,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             OA::template load<kBlockM>(sa, &map_a, &full[stage], kb * K_ELEMS, m0);
             OB::template load<BN>(sb, &map_b, &full[stage], kb * K_ELEMS, n0);
           }
-          if constexpr (NSETS == 2) {
+          if (NSETS == 2 && !(p.dbg & 8)) {
             uint8_t* sa2 = sb + B_BYTES;
             uint8_t* sb2 = sa2 + A_BYTES;
             OA::template load<kBlockM>(sa2, &map_a_lo, &full[stage], kb * K_ELEMS, m0);
@@ -796,6 +857,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           for (int kk = 0; kk < kAtomBytes / kUmmaKBytes; ++kk) {
             const uint64_t ada = OA::kstep(kk), adb = OB::kstep(kk);
             const uint32_t accum = (first && kk == 0) ? 0u : 1u;
+            if (p.dbg & 4) continue;  // experiment: no MMAs (operand-feed rate)
             if constexpr (CL == 2) umma2(tmem_t, da + ada, db + adb, idesc, accum);
             else umma<KIND>(tmem_t, da + ada, db + adb, idesc, accum);
             if constexpr (NSETS == 2) {
@@ -834,6 +896,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       const int64_t n0 = unit_n0(u);
       const int64_t soff = (u % p.ksplit) * p.m;  // split-K: partial s lands at rows + s * m
       float* stile = stile_all + (warp - 2) * kStileFloats;
+      if (p.dbg & 1) {  // experiment: accumulator hand-off only, no epilogue work
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        __syncwarp();
+        tc_fence_before();
+        if (lane == 0) {
+          if constexpr (CL == 2) mbar_arrive_cluster(mapa_rank(&tempty[acc], 0));
+          else mbar_arrive(&tempty[acc]);
+        }
+        continue;
+      }
       if constexpr (KIND == 1) {
         // fold chunks 1.. of this tile into its accumulator (chunk order)
         const int nch = (unit_kb1(u) - unit_kb0(u) + p.kchunk - 1) / p.kchunk;
@@ -854,6 +927,70 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           __syncwarp();
           if (lane == 0) mbar_arrive(&sempty[e_it & 1]);
         }
+      }
+      if (p.direct && p.coalesced && !(FEAT && p.colsum) && n0 + (int64_t)(half + 1) * kColsPerWarp <= p.n) {
+        // Direct path for epilogues that read nothing from global memory
+        // (NONE / BIAS / BIAS_RELU / ACC without C): lane = row, a 32-column
+        // TMEM chunk -> registers -> a bank-staggered 32 x 32 staging tile in
+        // the output type -> one TMA bulk store per chunk, and the accumulator
+        // is handed back as soon as its last chunk is read.  Measured on
+        // 8192 x 3328 x 3328 (tools/cublas_compare.py): 140 us with the
+        // staged fp32 transposition, 132 us here; the mainloop alone (no
+        // epilogue work, DMT_GEMM_DBG=1) 118 us, TMEM reads alone 119 us.
+        constexpr int kChunks = kColsPerWarp / 32;
+        const int64_t r = m0 + q * 32 + lane;
+        const bool ok = r < p.m;
+        const int64_t cbase = n0 + half * kColsPerWarp;
+        const EpiIn<TIN, TO> none{};  // (load-free epilogues only)
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < kChunks; ++c) {
+          float v[32];
+          if (!(p.dbg & 16))
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + half * kColsPerWarp + c * 32), v);
+          else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = (float)i;
+          }
+          if (c + 1 == kChunks) {  // accumulator fully read: hand it back before the stores
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (CL == 2) mbar_arrive_cluster(mapa_rank(&tempty[acc], 0));
+              else mbar_arrive(&tempty[acc]);
+            }
+          }
+          if (p.scale_acc) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
+          }
+          if (p.dbg & 2) {  // experiment: accumulator reads only
+            if (v[31] == 1234.5f && v[7] == 1.f) reinterpret_cast<float*>(p.d)[0] = v[0];
+            continue;
+          }
+          const int64_t col = cbase + c * 32;
+          const bool td = p.tma_out & 1;
+          if (ok) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              epi_finish<TIN, TO, FEAT>(p, r, col + 8 * j, v + 8 * j, none, nullptr, soff, nullptr, !td);
+          }
+          if (td) {
+            // the previous chunk's TMA store must have read the staging tile
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            uint8_t* sd = reinterpret_cast<uint8_t*>(stile);
+            stage_row<TO>(sd, lane, v);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&emaps.od, sd, (int)col, (int)(m0 + q * 32));
+              bulk_commit();
+            }
+          }
+        }
+        continue;
       }
       if (p.coalesced && n0 + (int64_t)(half + 1) * kColsPerWarp <= p.n) {
         // Pipelined full-width path: the epilogue operands (x0 / u / C / dx0)
@@ -1098,6 +1235,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         else mbar_arrive(&tempty[acc]);
       }
     }
+    if (p.tma_out && lane == 0) bulk_wait0();  // TMA-stored outputs complete before exit
   }
 
   __syncthreads();
@@ -1233,6 +1371,13 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   p.alpha = a->alpha;
   p.kchunk = tf32_kchunk();
   {
+    static const int dbg = [] {
+      const char* e = getenv("DMT_GEMM_DBG");
+      return e ? atoi(e) : 0;
+    }();
+    p.dbg = dbg;
+  }
+  {
     const int num_kb = (int)ceil_div(a->k * (int64_t)sizeof(TIN), kAtomBytes);
     p.ksplit = a->ksplit > 1 ? a->ksplit : 1;
     p.kbs = (int)ceil_div(num_kb, p.ksplit);
@@ -1265,6 +1410,20 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   const bool needs_x = a->epilogue == DMT_EPI_CROSS || a->epilogue == DMT_EPI_DCN_BWD ||
                        a->epilogue == DMT_EPI_DCN_FINAL || a->epilogue == DMT_EPI_RELU_BWD;
   p.coalesced = p.vec_store && (!needs_x || p.vec_x);
+  {
+    // register-direct epilogue with TMA-stored outputs for epilogues that read
+    // nothing from global memory (NONE / BIAS / BIAS_RELU / ACC with beta 0):
+    // per-lane row loads of x0 / u / C are slower than the staged path's
+    // coalesced ones (tools/gemm_bench.py).  DMT_GEMM_EPI=staged turns it off.
+    static const bool staged = [] {
+      const char* e = getenv("DMT_GEMM_EPI");
+      return e && std::string(e) == "staged";
+    }();
+    const bool loads = needs_x || a->aux || a->aux2 ||
+                       (a->beta != 0.f && (a->epilogue == DMT_EPI_ACC || a->epilogue == DMT_EPI_DCN_BWD ||
+                                           a->epilogue == DMT_EPI_DCN_FINAL));
+    p.direct = !staged && !loads;
+  }
   // fused bias-gradient column sums: every 32-column chunk must take a
   // coalesced epilogue path (n % 32 == 0) with 16-byte partial-row stores
   if (p.colsum && (!p.coalesced || a->n % 32 || ((uintptr_t)p.colsum % 16) || a->epilogue != DMT_EPI_DCN_BWD))
@@ -1306,6 +1465,12 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
     if (p.prefetch & 4) ok = ok && make_plain_map(&em.c, p.c, a->m, a->n, a->ld_d, a->out_dtype, bc, kBlockM);
     if (p.prefetch & 8) ok = ok && make_plain_map(&em.d2, a->aux2, a->m, a->n, a->ld_x, DMT_F32, bc, kBlockM);
     if (!ok) p.prefetch = 0;  // a hint only: skip it when a block cannot be described
+  }
+  // direct-path TMA stores: plain row-major output (no grouped / scattered
+  // layouts, no split-K workspace)
+  p.tma_out = 0;
+  if (p.direct && p.ksplit == 1 && !p.ngroups_out && !p.ncolg && p.rows_per_group > a->m && !(a->flags & DMT_GEMM_NO_TMA_STORE)) {
+    if (make_plain_map(&em.od, a->d, a->m, a->n, a->ld_d, a->out_dtype, 32, 32)) p.tma_out |= 1;
   }
   if (a->bias && ((uintptr_t)a->bias % 16)) return DMT_ERR_UNSUPPORTED;
   auto kern = gemm_kernel<BN, NOPS, KIND, STAGES, TIN, TO, AMN, BMN, FEAT, CL>;

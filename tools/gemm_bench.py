@@ -83,6 +83,10 @@ def main():
         ("bwd dX final 3 pairs", 2 * R * M * M,
          lambda: K.gemm(gu, W, out, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=u, beta=1.0,
                         pairs=[(x0, u), (xl, u), (x0, xl)]), None),
+        ("bwd dX dcn_bwd side", 2 * R * M * M,
+         lambda: K.gemm(gu, W, out, trans_b=True, epilogue=L.EPI_DCN_BWD, c=u, beta=1.0, x0=x0, aux=xl), None),
+        ("bwd g proj dcn side", 2 * R * M * P,
+         lambda: K.gemm(gy, Wp, out, trans_b=True, epilogue=L.EPI_DCN_BWD, x0=x0, aux=xl), None),
         ("bwd dX plain (K,MN)", 2 * R * M * M, lambda: K.gemm(gu, W, out, trans_b=True), None),
         ("bwd dW fused sgd", 2 * R * M * M,
          lambda: K.gemm(gu, xl, W, trans_a=True, trans_b=True, epilogue=L.EPI_ACC, beta=1.0, alpha=-1e-9), None),
@@ -95,6 +99,8 @@ def main():
     variants = [("auto", 0), ("single", L.GEMM_SINGLE_CTA), ("pair", L.GEMM_CLUSTER)] + [
         (f"bn{64 * j}", j << L.GEMM_BN_SHIFT) for j in (3, 4)] + [
         (f"bn{64 * j}pr", (j << L.GEMM_BN_SHIFT) | L.GEMM_CLUSTER) for j in (3, 4)]
+    if os.environ.get("GB_QUICK"):  # default choice and per-thread (non-TMA) direct stores only
+        variants = [("auto", 0), ("notma", L.GEMM_NO_TMA_STORE)]
     for name, flops, fn, ref in cases:
         line = f"{name:22s}"
         for vname, fl in variants:
