@@ -370,6 +370,19 @@ int dmt_cross_bwd_pointwise(const void* g, const void* x0, const void* u, void* 
 int dmt_dcn_dx0_term(const void* g, const void* u, float* dx0, int64_t n, int32_t dtype, int32_t accumulate,
                      dmt_stream_t stream);
 
+/* Fused element-wise tail of the crossnet backward, one pass over the saved
+ * layer tensors (16-bit dtype, all [rows, cols] contiguous, cols % 8 == 0,
+ * 1 <= nlayers <= 4):
+ *   dx0 = sum_{l = nlayers-1 .. 0} g[l] * u[l]        (fp32; the order of
+ *         dmt_dcn_dx0_term's sequence: bit-identical)
+ *   colsums[l][c] = sum_r gu[l][r, c]                  (= dmt_column_sum)
+ * Replaces nlayers dx0 terms plus nlayers column sums (derivative of
+ * towermod.py:132-139; the reference has no backward). */
+size_t dmt_dcn_side_fused_workspace_size(int64_t rows, int64_t cols, int32_t nlayers);
+int dmt_dcn_side_fused(const void* const* g, const void* const* u, const void* const* gu, int32_t nlayers,
+                       int64_t rows, int64_t cols, float* dx0, float* const* colsums, int32_t dtype,
+                       void* workspace, size_t workspace_bytes, dmt_stream_t stream);
+
 /* w -= lr * g  (w in dtype, g fp32), n elements */
 /* Loss head of the full DCN + SPTT training step (the reference has no
  * training): binary cross-entropy on logits z[n],

@@ -113,6 +113,9 @@ _SIGS = {
     "dmt_column_sum_parts": (C.c_int, [vp, i64, i64, vp, vp]),
     "dmt_cross_bwd_pointwise": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, vp]),
     "dmt_dcn_dx0_term": (C.c_int, [vp, vp, vp, i64, i32, i32, vp]),
+    "dmt_dcn_side_fused_workspace_size": (sz, [i64, i64, i32]),
+    "dmt_dcn_side_fused": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), i32, i64,
+                                     i64, vp, C.POINTER(C.c_void_p), i32, vp, sz, vp]),
     "dmt_sgd_dense": (C.c_int, [vp, vp, i64, f32, i32, vp]),
     "dmt_peer_sum_sgd": (C.c_int, [vp, C.POINTER(C.c_void_p), i32, i64, f32, i32, vp]),
     "dmt_peer_barrier": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), i32, vp, vp]),

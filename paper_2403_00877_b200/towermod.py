@@ -160,6 +160,11 @@ class TowerModule:
     #   "pairs": no dx0, every g_l kept, pair-sum final epilogue, bias-gradient
     #     column sums fused into the epilogues (L <= 4).
     dcn_bwd_form = os.environ.get("DMT_DCN_BWD", "side")
+    # side form: the element-wise tail (dx0 terms + crossnet bias column sums)
+    # as one fused pass after the layer-1 dX GEMM (default), or per layer
+    # beside each dW GEMM (DMT_DCN_SIDE=split; measured ~0.2 ms serialised
+    # behind the persistent GEMMs at C2: those kernels cannot co-reside)
+    _side_fused = os.environ.get("DMT_DCN_SIDE", "fused") == "fused"
 
     """Device TM of one tower: forward / backward / SGD on libdmt GEMMs.
 
@@ -402,8 +407,21 @@ class TowerModule:
         bias = {f"b{l}": torch.empty(M, dtype=torch.float32, device=dev) for l in range(L_)}
         bias["b_proj"] = torch.empty(gy.shape[1], dtype=torch.float32, device=dev)
 
+        fused = self._side_fused and dt in (torch.bfloat16, torch.float16) and M % 8 == 0 and 1 <= L_ <= 4
+
         def side_work(layer):
             # g_{layer+1} and gu_layer exist (written by the dX GEMM just issued)
+            if fused:
+                # one pass once every g_l / gu_l exists (after the layer-1 dX
+                # GEMM): all dx0 terms + all crossnet bias column sums
+                if layer != 0:
+                    return
+                side.wait_stream(main)
+                with torch.cuda.stream(side):
+                    K.dcn_side_fused([G[l + 1] for l in range(L_)], [us[l] for l in range(L_)], gu, dx0,
+                                     [bias[f"b{l}"] for l in range(L_)])
+                    K.column_sum(gy, out=bias["b_proj"])
+                return
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 K.dcn_dx0_term(G[layer + 1], us[layer], dx0, accumulate=layer != L_ - 1)

@@ -288,6 +288,32 @@ def test_column_sum_vs_fp64(rows, cols, dt):
     assert (got.double() - want).abs().max().item() <= 1e-5 * (x.double().abs().sum(0).max().item() + 1)
 
 
+@pytest.mark.parametrize("rows,cols,nl", [(8192, 3328, 3), (1000, 256, 2), (77, 64, 1), (130, 1664, 4)])
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+def test_dcn_side_fused_matches_separate_kernels(rows, cols, nl, dt):
+    """The fused crossnet-backward tail (dx0 = sum_{l=L-1..0} g_l u_l and the
+    bias column sums of gu_l, one pass) is bit-identical to the per-layer
+    dmt_dcn_dx0_term sequence plus dmt_column_sum (the DMT_DCN_SIDE=split form)
+    and within fp32 rounding of a float64 reference."""
+    from paper_2403_00877_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(rows * 7 + nl)
+    mk = lambda: torch.randn(rows, cols, device="cuda", generator=g).to(dt)  # noqa: E731
+    gs, us, gus = [mk() for _ in range(nl)], [mk() for _ in range(nl)], [mk() for _ in range(nl)]
+    dx0 = torch.full((rows, cols), float("nan"), device="cuda")
+    sums = [torch.full((cols,), float("nan"), device="cuda") for _ in range(nl)]
+    K.dcn_side_fused(gs, us, gus, dx0, sums)
+    want = torch.empty(rows, cols, device="cuda")
+    for l in range(nl - 1, -1, -1):
+        K.dcn_dx0_term(gs[l], us[l], want, accumulate=l != nl - 1)
+    torch.cuda.synchronize()
+    assert torch.equal(dx0, want)
+    for l in range(nl):
+        assert torch.equal(sums[l], K.column_sum(gus[l]))
+    ref = sum(gs[l].double() * us[l].double() for l in range(nl))
+    assert (dx0.double() - ref).abs().max().item() <= 1e-6 * (ref.abs().max().item() + 1)
+
+
 @pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("nsrc,n", [(1, 5), (2, 1664 * 1664 + 3), (3, 4096), (4, 832)])
 def test_peer_sum_sgd_matches_rank_order_sum(dt, nsrc, n):
