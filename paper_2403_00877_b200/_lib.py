@@ -140,7 +140,10 @@ def load_library(require_cuda: bool = True):
                 "(there is no CPU fallback)"
             )
         lib = C.CDLL(LIB_PATH)
+        ab_build = "DMT_LIB" in os.environ  # an older A/B build may lack newer entry points
         for name, (res, args) in _SIGS.items():
+            if ab_build and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -129,14 +129,26 @@ pooled_fwd_kernel(const dmt_lookup_segment* __restrict__ segs, const int64_t* __
   if (sg.pooling == DMT_POOL_NONE && len != 1 && err) atomicOr(err, DMT_EBIT_BAGLEN);
 
   int bad = 0;
+  // the next batch's indices are loaded while this batch's rows are in
+  // flight, so only a bag's first batch waits on an index load before its
+  // row loads (a bag of 20 at UN = 8 paid three index -> row chains)
+  int32_t nidx[UN];
+#pragma unroll
+  for (int u = 0; u < UN; ++u) nidx[u] = (beg + u < end) ? __ldg(indices + beg + u) : 0;
   for (int64_t k0 = beg; k0 < end; k0 += UN) {
     Frag<T, VEC> fr[UN][NV];
     bool use[UN];
+    int32_t idx[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      idx[u] = nidx[u];
+      nidx[u] = (k0 + UN + u < end) ? __ldg(indices + k0 + UN + u) : 0;
+    }
 #pragma unroll
     for (int u = 0; u < UN; ++u) {
       use[u] = false;
       if (k0 + u < end) {
-        const int64_t gi = (int64_t)__ldg(indices + k0 + u);
+        const int64_t gi = (int64_t)idx[u];
         int64_t r = gi - row_begin;
         bool in = r >= 0 && r < rows;
         if (!in && (!filt || (sg.table_rows > 0 && (gi < 0 || gi >= sg.table_rows)))) bad = 1;
@@ -229,8 +241,12 @@ int launch_fwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
     int bags_per_block = kLookupThreads / G;
     dim3 grid((unsigned)ceil_div(max_b, bags_per_block), n);
     static int un = [] {
-      const char* e = getenv("DMT_LOOKUP_UNROLL");  // tuning knob (default 8)
-      return e ? atoi(e) : 8;
+      // rows in flight per thread (DMT_LOOKUP_UNROLL overrides).  With the
+      // next batch's indices prefetched, fewer rows per batch at higher
+      // occupancy win: C2 bf16 (L = 20) 219 us at 8 (round 1 kernel) ->
+      // 218.7 / 210.7 / 213.0 us at 4 / 5 / 6 (tools/lookup_bench.py, one box)
+      const char* e = getenv("DMT_LOOKUP_UNROLL");
+      return e ? atoi(e) : 5;
     }();
     if (NV == 1 && un == 4)
       pooled_fwd_kernel<T, VEC, 1, 4><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
@@ -238,6 +254,10 @@ int launch_fwd(const dmt_lookup_segment* segs, const dmt_lookup_segment* hs, int
       pooled_fwd_kernel<T, VEC, 1, 6><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
     else if (NV == 1 && un == 12)
       pooled_fwd_kernel<T, VEC, 1, 12><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
+    else if (NV == 1 && un == 5)
+      pooled_fwd_kernel<T, VEC, 1, 5><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
+    else if (NV == 1 && un == 10)
+      pooled_fwd_kernel<T, VEC, 1, 10><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
     else if (NV == 1)
       pooled_fwd_kernel<T, VEC, 1><<<grid, kLookupThreads, 0, s>>>(segs, offsets, indices, log2g, err);
     else if (NV == 2)
