@@ -370,8 +370,10 @@ int dmt_cross_bwd_pointwise(const void* g, const void* x0, const void* u, void* 
 int dmt_dcn_dx0_term(const void* g, const void* u, float* dx0, int64_t n, int32_t dtype, int32_t accumulate,
                      dmt_stream_t stream);
 
-/* Fused element-wise tail of the crossnet backward, one pass over the saved
- * layer tensors (16-bit dtype, all [rows, cols] contiguous, cols % 8 == 0,
+/* Element-wise tail of the crossnet backward after the last per-layer dX
+ * GEMM: dx0 in one streaming pass over the saved layer tensors (instead of
+ * nlayers fp32 read-modify-write passes), then the bias column sums
+ * (16-bit dtype, all [rows, cols] contiguous, cols % 8 == 0,
  * 1 <= nlayers <= 4):
  *   dx0 = sum_{l = nlayers-1 .. 0} g[l] * u[l]        (fp32; the order of
  *         dmt_dcn_dx0_term's sequence: bit-identical)

@@ -292,46 +292,35 @@ __global__ void dcn_dx0_term_kernel(const T* __restrict__ g, const T* __restrict
   }
 }
 
-// Fused element-wise tail of the crossnet backward: one pass over the saved
-// layer tensors instead of L dx0 terms (fp32 read-modify-write each) plus L
-// column sums -- 9 x 54.5 MB read + 109 MB written at C2 instead of ~1.07 GB.
-// Thread = (8 columns, row slice p of colsum_parts); per element
-//   dx0 = sum_{l = L-1..0} g_l * u_l           (fp32, the dx0-term order)
-//   part_l[p, c] = sum over the slice of gu_l   (fp32 per 32 rows folded into
-//                                                fp64: colsum_partial_vec's order)
-// so dx0 and the bias gradients are bit-identical to the separate kernels.
+// Element-wise tail of the crossnet backward in one streaming pass:
+//   dx0 = sum_{l = L-1..0} g_l * u_l   (fp32, the dx0-term order: bit-identical)
+// reading each g_l / u_l once and writing dx0 once (2 L x 54.5 MB + 109 MB at
+// C2) instead of L read-modify-write passes over the fp32 dx0.  A single pass
+// that also column-summed gu_l (thread = 8 columns x a 64-row slice, the
+// column-sum partial layout) measured latency bound at 3.3 TB/s (181 us);
+// this flat grid-stride form streams like dmt_dcn_dx0_term.
 struct SidePtrs {
   const void* g[4];
   const void* u[4];
-  const void* gu[4];
 };
 
 template <typename T, int NL>
-__global__ void __launch_bounds__(64) dcn_side_fused_kernel(const SidePtrs P, int64_t rows, int64_t cols,
-                                                            int64_t rows_per, float* __restrict__ dx0,
-                                                            double* __restrict__ parts) {
-  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (c >= cols) return;
-  const int64_t r0 = (int64_t)blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
+__global__ void __launch_bounds__(256) dcn_dx0_sum_kernel(const SidePtrs P, int64_t n, float* __restrict__ dx0) {
+  const int64_t nv = n / 8;
   const T* g[NL];
   const T* u[NL];
-  const T* gu[NL];
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
     g[l] = reinterpret_cast<const T*>(P.g[l]);
     u[l] = reinterpret_cast<const T*>(P.u[l]);
-    gu[l] = reinterpret_cast<const T*>(P.gu[l]);
   }
-  float acc[NL][8];
-  double dacc[NL][8];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    uint4 gr[NL], ur[NL];
 #pragma unroll
-  for (int l = 0; l < NL; ++l)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) { acc[l][e] = 0.f; dacc[l][e] = 0.0; }
-  // two rows per step: all 2 * 3 * NL loads are issued before either row is
-  // consumed (one row at a time measured latency bound: 243 us at C2)
-  int cnt = 0;
-  auto row = [&](const uint4* gr, const uint4* ur, const uint4* qr, int64_t o) {
+    for (int l = 0; l < NL; ++l) {
+      gr[l] = __ldg(reinterpret_cast<const uint4*>(g[l] + i * 8));
+      ur[l] = __ldg(reinterpret_cast<const uint4*>(u[l] + i * 8));
+    }
     float d[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) d[e] = 0.f;
@@ -342,54 +331,9 @@ __global__ void __launch_bounds__(64) dcn_side_fused_kernel(const SidePtrs P, in
 #pragma unroll
       for (int e = 0; e < 8; ++e) d[e] += to_f<T>(gh[e]) * to_f<T>(uh[e]);
     }
-    *reinterpret_cast<float4*>(dx0 + o) = make_float4(d[0], d[1], d[2], d[3]);
-    *reinterpret_cast<float4*>(dx0 + o + 4) = make_float4(d[4], d[5], d[6], d[7]);
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      const T* qh = reinterpret_cast<const T*>(&qr[l]);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[l][e] += to_f<T>(qh[e]);
-    }
-    if (++cnt == 32) {
-#pragma unroll
-      for (int l = 0; l < NL; ++l)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) { dacc[l][e] += acc[l][e]; acc[l][e] = 0.f; }
-      cnt = 0;
-    }
-  };
-  int64_t r = r0;
-  for (; r + 2 <= r1; r += 2) {
-    const int64_t o0 = r * cols + c, o1 = o0 + cols;
-    uint4 gr[2][NL], ur[2][NL], qr[2][NL];
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      gr[0][l] = __ldg(reinterpret_cast<const uint4*>(g[l] + o0));
-      ur[0][l] = __ldg(reinterpret_cast<const uint4*>(u[l] + o0));
-      qr[0][l] = __ldg(reinterpret_cast<const uint4*>(gu[l] + o0));
-      gr[1][l] = __ldg(reinterpret_cast<const uint4*>(g[l] + o1));
-      ur[1][l] = __ldg(reinterpret_cast<const uint4*>(u[l] + o1));
-      qr[1][l] = __ldg(reinterpret_cast<const uint4*>(gu[l] + o1));
-    }
-    row(gr[0], ur[0], qr[0], o0);
-    row(gr[1], ur[1], qr[1], o1);
+    *reinterpret_cast<float4*>(dx0 + i * 8) = make_float4(d[0], d[1], d[2], d[3]);
+    *reinterpret_cast<float4*>(dx0 + i * 8 + 4) = make_float4(d[4], d[5], d[6], d[7]);
   }
-  if (r < r1) {
-    const int64_t o0 = r * cols + c;
-    uint4 gr[NL], ur[NL], qr[NL];
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      gr[l] = __ldg(reinterpret_cast<const uint4*>(g[l] + o0));
-      ur[l] = __ldg(reinterpret_cast<const uint4*>(u[l] + o0));
-      qr[l] = __ldg(reinterpret_cast<const uint4*>(gu[l] + o0));
-    }
-    row(gr, ur, qr, o0);
-  }
-  const int64_t np = gridDim.y;
-#pragma unroll
-  for (int l = 0; l < NL; ++l)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) parts[((int64_t)l * np + blockIdx.y) * cols + c + e] = dacc[l][e] + acc[l][e];
 }
 
 template <typename T>
@@ -658,13 +602,11 @@ int dmt_dcn_side_fused(const void* const* g, const void* const* u, const void* c
     if ((((uintptr_t)g[l] | (uintptr_t)u[l] | (uintptr_t)gu[l]) & 15) || !colsums[l]) return DMT_ERR_DOMAIN;
   if (workspace_bytes < dmt_dcn_side_fused_workspace_size(rows, cols, nlayers)) return DMT_ERR_DOMAIN;
   cudaStream_t s = (cudaStream_t)stream;
-  const int nparts = colsum_parts(rows);
-  const int64_t rows_per = dmt::ceil_div(rows, nparts);
-  double* parts = (double*)workspace;
   dmt::SidePtrs P = {};
-  for (int l = 0; l < nlayers; ++l) { P.g[l] = g[l]; P.u[l] = u[l]; P.gu[l] = gu[l]; }
-  dim3 grid((unsigned)dmt::ceil_div(cols / 8, 64), nparts);
-#define DMT_SIDE(T, NL) dmt::dcn_side_fused_kernel<T, NL><<<grid, 64, 0, s>>>(P, rows, cols, rows_per, dx0, parts)
+  for (int l = 0; l < nlayers; ++l) { P.g[l] = g[l]; P.u[l] = u[l]; }
+  const int64_t n = rows * cols;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(dmt::ceil_div(n / 8, 256), DMT_NUM_SMS * 8));
+#define DMT_SIDE(T, NL) dmt::dcn_dx0_sum_kernel<T, NL><<<grid, 256, 0, s>>>(P, n, dx0)
   if (dtype == DMT_BF16) {
     switch (nlayers) {
       case 1: DMT_SIDE(__nv_bfloat16, 1); break;
@@ -681,9 +623,12 @@ int dmt_dcn_side_fused(const void* const* g, const void* const* u, const void* c
     }
   }
 #undef DMT_SIDE
-  for (int l = 0; l < nlayers; ++l)
-    dmt::colsum_final<<<(unsigned)dmt::ceil_div(cols, 32), 256, 0, s>>>(parts + (size_t)l * nparts * cols, cols, nparts,
-                                                                        colsums[l]);
+  // bias gradients: the dmt_column_sum kernels (same partials, same order)
+  const size_t per = sizeof(double) * (size_t)colsum_parts(rows) * (size_t)cols;
+  for (int l = 0; l < nlayers; ++l) {
+    const int rc = dmt_column_sum(gu[l], rows, cols, cols, colsums[l], dtype, (char*)workspace + l * per, per, stream);
+    if (rc != DMT_OK) return rc;
+  }
   DMT_CHECK_LAUNCH();
   return DMT_OK;
 }

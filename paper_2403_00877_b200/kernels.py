@@ -538,7 +538,8 @@ def dcn_dx0_term(g: torch.Tensor, u: torch.Tensor, dx0: torch.Tensor, accumulate
 
 def dcn_side_fused(gs: list, us: list, gus: list, dx0: torch.Tensor, colsums: list) -> None:
     """dx0 = sum_{l=L-1..0} gs[l] * us[l] (fp32) and colsums[l] = column sums of
-    gus[l], in one pass (bit-identical to dcn_dx0_term + column_sum)."""
+    gus[l]: dx0 in one streaming pass, then the column sums (bit-identical to
+    the dcn_dx0_term sequence + column_sum)."""
     import ctypes as C
 
     n = len(gs)
