@@ -1410,11 +1410,80 @@ constexpr size_t kRadixDownSmem = (size_t)kRadixWarps * kRadixStreams * kRadixBi
 
 inline int64_t radix_tiles(int64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
 
+// Exclusive scan of the digit-major (digit, tile) counts: tile sums, then each
+// block adds the sums of the tiles before it and scans its own 4096 counts
+// (two launches; replaces the CUB DeviceScan of round 1).  The count arrays
+// are multiples of kRadixBins long, so whole 16-byte vectors.
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kRadixThreads * kScanItems;  // 1024
+
+__device__ __forceinline__ uint32_t block_sum_u32(uint32_t v, uint32_t* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  uint32_t t = 0;
+  for (int i = 0; i < kRadixWarps; ++i) t += red[i];
+  return t;
+}
+
+__global__ void __launch_bounds__(kRadixThreads) scan_u32_tile_sums(const uint32_t* __restrict__ in, int64_t n,
+                                                                    uint32_t* __restrict__ sums) {
+  __shared__ uint32_t red[kRadixWarps];
+  const int64_t i0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t v = 0;
+  if (i0 < n) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(in + i0));
+    v = x.x + x.y + x.z + x.w;
+  }
+  v = block_sum_u32(v, red);
+  if (threadIdx.x == 0) sums[blockIdx.x] = v;
+}
+
+__global__ void __launch_bounds__(kRadixThreads) scan_u32_tiles(const uint32_t* __restrict__ in, int64_t n,
+                                                                const uint32_t* __restrict__ sums,
+                                                                uint32_t* __restrict__ out) {
+  __shared__ uint32_t red[kRadixWarps];
+  __shared__ uint32_t wsum[kRadixWarps];
+  uint32_t p = 0;
+  for (int i = threadIdx.x; i < (int)blockIdx.x; i += kRadixThreads) p += __ldg(sums + i);
+  const uint32_t prefix = block_sum_u32(p, red);
+  // thread t scans items [t * 4, t * 4 + 4) of the tile
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t x[kScanItems] = {0u, 0u, 0u, 0u};
+  if (base < n) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(in + base));
+    x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w;
+  }
+  uint32_t tsum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) tsum += x[i];
+  // exclusive scan of the thread totals: warp inclusive scan + warp offsets
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  uint32_t inc = tsum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (l >= o) inc += y;
+  }
+  if (l == 31) wsum[w] = inc;
+  __syncthreads();
+  uint32_t woff = 0;
+  for (int i = 0; i < w; ++i) woff += wsum[i];
+  uint32_t run = prefix + woff + inc - tsum;
+  if (base < n) {
+    uint4 o;
+    o.x = run; run += x[0];
+    o.y = run; run += x[1];
+    o.z = run; run += x[2];
+    o.w = run;
+    *reinterpret_cast<uint4*>(out + base) = o;
+  }
+}
+
 inline size_t radix_scan_bytes(int64_t n) {
-  size_t bytes = 0;
   const int64_t items = radix_tiles(std::max<int64_t>(n, 1)) * kRadixBins;
-  cub::DeviceScan::ExclusiveSum((void*)nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)items);
-  return bytes;
+  return sizeof(uint32_t) * (size_t)((items + kScanTile - 1) / kScanTile);
 }
 
 // Sorts n pairs by the low end_bit bits of the keys; the result lands in the
@@ -1441,8 +1510,10 @@ inline int radix_sort_pairs(uint32_t* keys_in, int32_t* vals_in, uint32_t* keys_
     const int shift = pass * db;
     radix_upsweep<<<(unsigned)nt, kRadixThreads, 0, s>>>(ki, n, shift, mask, nt, counts);
     DMT_CHECK_LAUNCH();
-    size_t sb = scan_bytes;
-    if (cub::DeviceScan::ExclusiveSum(scan_tmp, sb, counts, offsets, items, s) != cudaSuccess) return DMT_ERR_CUDA;
+    const unsigned st = (unsigned)((items + kScanTile - 1) / kScanTile);
+    if (scan_bytes < st * sizeof(uint32_t)) return DMT_ERR_DOMAIN;
+    scan_u32_tile_sums<<<st, kRadixThreads, 0, s>>>(counts, items, (uint32_t*)scan_tmp);
+    scan_u32_tiles<<<st, kRadixThreads, 0, s>>>(counts, items, (const uint32_t*)scan_tmp, offsets);
     radix_downsweep<<<(unsigned)nt, kRadixThreads, kRadixDownSmem, s>>>(ki, vi, ko, vo, n, shift, db, nt, offsets);
     DMT_CHECK_LAUNCH();
     std::swap(ki, ko);
