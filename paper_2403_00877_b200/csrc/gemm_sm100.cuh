@@ -315,6 +315,7 @@ struct Params {
   int ksplit;     // split-K: units = tiles x ksplit; split s covers K blocks [s*kbs, (s+1)*kbs)
   int kbs;        //   and writes its raw fp32 accumulator at output rows + s * m (workspace)
   int tma_out;    // direct path: bit 0 = output stored by TMA (emaps.od)
+  int pf_ahead;   // staged epilogue: L2-prefetch the operands this many slabs ahead (0 = off)
   int direct;     // register-direct epilogue (no shared-memory staging); DMT_GEMM_EPI=staged turns it off
   int dbg;        // experiment only (DMT_GEMM_DBG): 1 skip epilogue work, 2 / 16 direct epilogue without
                   // stores / TMEM loads, 4 skip MMAs, 8 skip TMA loads
@@ -502,6 +503,21 @@ __device__ __forceinline__ void epi_load(const Params& p, int64_t row, int64_t c
     rawld(reinterpret_cast<const TO*>(p.c) + row * p.ld_d + col, in.c);
   if ((e == DMT_EPI_DCN_FINAL && !(FEAT ? p.npairs : 0)) || (e == DMT_EPI_DCN_BWD && p.aux2 && p.aux2_accum))
     rawld(p.aux2 + xo, in.d);
+}
+
+// L2 prefetch of one 8-column row piece's epilogue operands (no registers
+// held): issued a few slabs ahead of the register loads in the staged path.
+__device__ __forceinline__ void l2pf(const void* a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); }
+template <typename TIN, typename TO, bool FEAT>
+__device__ __forceinline__ void epi_prefetch(const Params& p, int64_t row, int64_t col) {
+  const int64_t xo = row * p.ld_x + col;
+  const int e = p.epilogue;
+  if (e == DMT_EPI_CROSS || e == DMT_EPI_DCN_BWD || e == DMT_EPI_RELU_BWD) l2pf(reinterpret_cast<const TIN*>(p.x0) + xo);
+  if (e == DMT_EPI_CROSS || (e == DMT_EPI_DCN_BWD && p.aux2)) l2pf(reinterpret_cast<const TIN*>(p.xl) + xo);
+  if ((e == DMT_EPI_ACC || e == DMT_EPI_DCN_BWD || e == DMT_EPI_DCN_FINAL) && p.beta != 0.f)
+    l2pf(reinterpret_cast<const TO*>(p.c) + row * p.ld_d + col);
+  if ((e == DMT_EPI_DCN_FINAL && !(FEAT ? p.npairs : 0)) || (e == DMT_EPI_DCN_BWD && p.aux2 && p.aux2_accum))
+    l2pf(p.aux2 + xo);
 }
 
 // dx0 = sum_l g_{l+1} * u_l straight from the saved layer tensors (DCN_FINAL).
@@ -1009,6 +1025,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           int64_t r, col;
           slab_pos(0, r, col);
           if (r < p.m) epi_load<TIN, TO, FEAT>(p, r, col, nx);
+          for (int k = 1; k < p.pf_ahead && k < kSlabs; ++k) {
+            slab_pos(k, r, col);
+            if (r < p.m) epi_prefetch<TIN, TO, FEAT>(p, r, col);
+          }
         }
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -1034,6 +1054,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             int64_t rn, coln;
             slab_pos(k + 1, rn, coln);
             if (rn < p.m) epi_load<TIN, TO, FEAT>(p, rn, coln, nx);
+          }
+          if (p.pf_ahead && k + p.pf_ahead < kSlabs) {
+            int64_t rp, colp;
+            slab_pos(k + p.pf_ahead, rp, colp);
+            if (rp < p.m) epi_prefetch<TIN, TO, FEAT>(p, rp, colp);
           }
           const int rl = (k & 3) * 8 + (lane >> 2);
           float a[8];
@@ -1376,6 +1401,15 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
       return e ? atoi(e) : 0;
     }();
     p.dbg = dbg;
+    // per-lane L2 prefetch of the staged epilogue's operands two slabs ahead:
+    // pays only on DCN_FINAL, whose fp32 dx0 operand doubles the bytes per
+    // piece (8192 x 3328 x 3328: 151 -> 137 us; CROSS / DCN_BWD / ACC +1-5 %,
+    // tools/gemm_bench.py).  DMT_EPI_PF_AHEAD=n forces n slabs (0 = off).
+    static const int pfa = [] {
+      const char* e = getenv("DMT_EPI_PF_AHEAD");
+      return e ? atoi(e) : -1;
+    }();
+    p.pf_ahead = pfa >= 0 ? pfa : ((a->epilogue == DMT_EPI_DCN_FINAL && a->aux2 && a->npairs == 0) ? 2 : 0);
   }
   {
     const int num_kb = (int)ceil_div(a->k * (int64_t)sizeof(TIN), kAtomBytes);
