@@ -314,7 +314,7 @@ struct Params {
   int64_t colg_ld[DMT_GEMM_MAX_COL_GROUPS];
   int ksplit;     // split-K: units = tiles x ksplit; split s covers K blocks [s*kbs, (s+1)*kbs)
   int kbs;        //   and writes its raw fp32 accumulator at output rows + s * m (workspace)
-  int tma_out;    // direct path: bit 0 = output stored by TMA (emaps.od)
+  int tma_out;    // direct path: bit 0 = output stored by TMA (emaps.od), bit 1 = 64-column boxes (emaps.od64)
   int pf_ahead;   // staged epilogue: L2-prefetch the operands this many slabs ahead (0 = off)
   int direct;     // register-direct epilogue (no shared-memory staging); DMT_GEMM_EPI=staged turns it off
   int dbg;        // experiment only (DMT_GEMM_DBG): 1 skip epilogue work, 2 / 16 direct epilogue without
@@ -639,6 +639,32 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// One row (this lane's) of a 32-column chunk of 16-bit outputs into half
+// `hf` of a 32 x 64 staging tile (128-byte rows: the TMA store then writes
+// whole 128-byte lines).  Rows are 128 B apart, so 8 lanes can cover only 4
+// distinct 16-byte bank groups per store: 2-way conflicts, accepted.
+template <typename T>
+__device__ __forceinline__ void stage_row64(uint8_t* buf, int lane, const float* v, int hf) {
+  static_assert(sizeof(T) == 2, "16-bit outputs");
+  uint4 ch[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    T* h = reinterpret_cast<T*>(&ch[c]);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) h[e] = from_f<T>(v[c * 8 + e]);
+  }
+  uint4* row = reinterpret_cast<uint4*>(buf + lane * 128) + hf * 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int idx = (j + lane) & 3;
+    uint4 x = ch[0];
+#pragma unroll
+    for (int c = 1; c < 4; ++c)
+      if (idx == c) x = ch[c];
+    row[idx] = x;
+  }
+}
+
 // One row (this lane's) of a 32 x 32 output chunk into an unswizzled staging
 // tile (row pitch 32 * sizeof(T)) for a TMA store.  Store j of lane r writes
 // 16-byte piece (j + s_r) mod P, s_r chosen so that every 8-lane phase covers
@@ -681,7 +707,8 @@ __device__ __forceinline__ void l2_prefetch_2d(const CUtensorMap* map, int c0, i
 
 struct EpiMaps {
   CUtensorMap x0, xl, c, d2;
-  CUtensorMap od;  // TMA store of the output (32 x 32 boxes)
+  CUtensorMap od;    // TMA store of the output (32 x 32 boxes)
+  CUtensorMap od64;  // 16-bit outputs: 32 rows x 64 columns (whole 128-byte lines)
 };
 
 constexpr int kStileFloats = 32 * 33;
@@ -992,7 +1019,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             for (int j = 0; j < 4; ++j)
               epi_finish<TIN, TO, FEAT>(p, r, col + 8 * j, v + 8 * j, none, nullptr, soff, nullptr, !td);
           }
-          if (td) {
+          if (td && sizeof(TO) == 2 && (p.tma_out & 2) && (kChunks % 2) == 0) {
+            // pairs of chunks into one 32 x 64 tile, one TMA store per pair
+            uint8_t* sd = reinterpret_cast<uint8_t*>(stile);
+            if ((c & 1) == 0) {
+              if (lane == 0) bulk_wait_read0();
+              __syncwarp();
+            }
+            if constexpr (sizeof(TO) == 2) stage_row64<TO>(sd, lane, v, c & 1);
+            if (c & 1) {
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&emaps.od64, sd, (int)(col - 32), (int)(m0 + q * 32));
+                bulk_commit();
+              }
+            }
+          } else if (td) {
             // the previous chunk's TMA store must have read the staging tile
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
@@ -1505,6 +1548,13 @@ static int launch(const dmt_gemm_args* a, const void* a_lo, const void* b_lo, cu
   p.tma_out = 0;
   if (p.direct && p.ksplit == 1 && !p.ngroups_out && !p.ncolg && p.rows_per_group > a->m && !(a->flags & DMT_GEMM_NO_TMA_STORE)) {
     if (make_plain_map(&em.od, a->d, a->m, a->n, a->ld_d, a->out_dtype, 32, 32)) p.tma_out |= 1;
+    static const bool wide = [] {
+      const char* e = getenv("DMT_GEMM_TMA64");
+      return !e || atoi(e) != 0;
+    }();
+    if ((p.tma_out & 1) && wide && sizeof(TO) == 2 &&
+        make_plain_map(&em.od64, a->d, a->m, a->n, a->ld_d, a->out_dtype, 64, 32))
+      p.tma_out |= 2;
   }
   if (a->bias && ((uintptr_t)a->bias % 16)) return DMT_ERR_UNSUPPORTED;
   auto kern = gemm_kernel<BN, NOPS, KIND, STAGES, TIN, TO, AMN, BMN, FEAT, CL>;
