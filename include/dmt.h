@@ -377,7 +377,8 @@ int dmt_dcn_dx0_term(const void* g, const void* u, float* dx0, int64_t n, int32_
  * 1 <= nlayers <= 4):
  *   dx0 = sum_{l = nlayers-1 .. 0} g[l] * u[l]        (fp32; the order of
  *         dmt_dcn_dx0_term's sequence: bit-identical)
- *   colsums[l][c] = sum_r gu[l][r, c]                  (= dmt_column_sum)
+ *   colsums[l][c] = sum_r gu[l][r, c]                  (= dmt_column_sum;
+ *                                                        colsums == NULL: dx0 only)
  * Replaces nlayers dx0 terms plus nlayers column sums (derivative of
  * towermod.py:132-139; the reference has no backward). */
 size_t dmt_dcn_side_fused_workspace_size(int64_t rows, int64_t cols, int32_t nlayers);

@@ -598,8 +598,10 @@ int dmt_dcn_side_fused(const void* const* g, const void* const* u, const void* c
   if (rows == 0 || cols == 0) return DMT_OK;
   if (dtype != DMT_BF16 && dtype != DMT_F16) return DMT_ERR_UNSUPPORTED;
   if (cols % 8 || ((uintptr_t)dx0 & 15)) return DMT_ERR_DOMAIN;
-  for (int l = 0; l < nlayers; ++l)
-    if ((((uintptr_t)g[l] | (uintptr_t)u[l] | (uintptr_t)gu[l]) & 15) || !colsums[l]) return DMT_ERR_DOMAIN;
+  for (int l = 0; l < nlayers; ++l) {
+    if (((uintptr_t)g[l] | (uintptr_t)u[l]) & 15) return DMT_ERR_DOMAIN;
+    if (colsums && (!gu || ((uintptr_t)gu[l] & 15) || !colsums[l])) return DMT_ERR_DOMAIN;
+  }
   if (workspace_bytes < dmt_dcn_side_fused_workspace_size(rows, cols, nlayers)) return DMT_ERR_DOMAIN;
   cudaStream_t s = (cudaStream_t)stream;
   dmt::SidePtrs P = {};
@@ -623,9 +625,10 @@ int dmt_dcn_side_fused(const void* const* g, const void* const* u, const void* c
     }
   }
 #undef DMT_SIDE
-  // bias gradients: the dmt_column_sum kernels (same partials, same order)
+  // bias gradients: the dmt_column_sum kernels (same partials, same order);
+  // colsums == NULL: dx0 only
   const size_t per = sizeof(double) * (size_t)colsum_parts(rows) * (size_t)cols;
-  for (int l = 0; l < nlayers; ++l) {
+  for (int l = 0; colsums && l < nlayers; ++l) {
     const int rc = dmt_column_sum(gu[l], rows, cols, cols, colsums[l], dtype, (char*)workspace + l * per, per, stream);
     if (rc != DMT_OK) return rc;
   }

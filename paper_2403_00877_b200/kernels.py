@@ -536,17 +536,18 @@ def dcn_dx0_term(g: torch.Tensor, u: torch.Tensor, dx0: torch.Tensor, accumulate
                                      L.stream_ptr()), "dmt_dcn_dx0_term")
 
 
-def dcn_side_fused(gs: list, us: list, gus: list, dx0: torch.Tensor, colsums: list) -> None:
+def dcn_side_fused(gs: list, us: list, gus: Optional[list], dx0: torch.Tensor, colsums: Optional[list]) -> None:
     """dx0 = sum_{l=L-1..0} gs[l] * us[l] (fp32) and colsums[l] = column sums of
     gus[l]: dx0 in one streaming pass, then the column sums (bit-identical to
     the dcn_dx0_term sequence + column_sum)."""
     import ctypes as C
 
     n = len(gs)
-    if not (1 <= n <= 4) or len(us) != n or len(gus) != n or len(colsums) != n:
-        raise ShapeError("dcn_side_fused: 1..4 layers, one g / u / gu / colsum each")
+    sums = colsums is not None
+    if not (1 <= n <= 4) or len(us) != n or (sums and (gus is None or len(gus) != n or len(colsums) != n)):
+        raise ShapeError("dcn_side_fused: 1..4 layers, one g / u (/ gu / colsum) each")
     rows, cols = gs[0].shape
-    for t in (*gs, *us, *gus):
+    for t in (*gs, *us, *(gus if sums else ())):
         if tuple(t.shape) != (rows, cols) or not t.is_contiguous() or t.dtype != gs[0].dtype:
             raise ShapeError("dcn_side_fused: contiguous [rows, cols] operands of one dtype")
     if dx0.dtype != torch.float32 or dx0.numel() != rows * cols or not dx0.is_contiguous():
@@ -555,9 +556,9 @@ def dcn_side_fused(gs: list, us: list, gus: list, dx0: torch.Tensor, colsums: li
                      device=dx0.device)
     arr = C.c_void_p * n
     L.check(L.lib().dmt_dcn_side_fused(arr(*[t.data_ptr() for t in gs]), arr(*[t.data_ptr() for t in us]),
-                                       arr(*[t.data_ptr() for t in gus]), n, rows, cols, dx0.data_ptr(),
-                                       arr(*[t.data_ptr() for t in colsums]), _dt(gs[0]), ws.data_ptr(),
-                                       ws.numel(), L.stream_ptr()), "dmt_dcn_side_fused")
+                                       arr(*[t.data_ptr() for t in gus]) if sums else None, n, rows, cols,
+                                       dx0.data_ptr(), arr(*[t.data_ptr() for t in colsums]) if sums else None,
+                                       _dt(gs[0]), ws.data_ptr(), ws.numel(), L.stream_ptr()), "dmt_dcn_side_fused")
 
 
 def sgd_dense(w: torch.Tensor, g: torch.Tensor, lr: float) -> None:

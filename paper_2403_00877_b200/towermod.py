@@ -165,6 +165,7 @@ class TowerModule:
     # beside each dW GEMM (DMT_DCN_SIDE=split; measured ~0.2 ms serialised
     # behind the persistent GEMMs at C2: those kernels cannot co-reside)
     _side_fused = os.environ.get("DMT_DCN_SIDE", "fused") == "fused"
+    _tail_main = os.environ.get("DMT_DCN_TAIL", "side") == "main"
 
     """Device TM of one tower: forward / backward / SGD on libdmt GEMMs.
 
@@ -416,6 +417,16 @@ class TowerModule:
                 # GEMM): all dx0 terms + all crossnet bias column sums
                 if layer != 0:
                     return
+                if self._tail_main:
+                    # dx0 on the main chain (the final dX GEMM needs it), the
+                    # bias column sums on the side stream, joined at the end
+                    K.dcn_side_fused([G[l + 1] for l in range(L_)], [us[l] for l in range(L_)], None, dx0, None)
+                    side.wait_stream(main)
+                    with torch.cuda.stream(side):
+                        for l in range(L_):
+                            K.column_sum(gu[l], out=bias[f"b{l}"])
+                        K.column_sum(gy, out=bias["b_proj"])
+                    return
                 side.wait_stream(main)
                 with torch.cuda.stream(side):
                     K.dcn_side_fused([G[l + 1] for l in range(L_)], [us[l] for l in range(L_)], gu, dx0,
@@ -443,11 +454,14 @@ class TowerModule:
             else:
                 # the side stream's last dx0 term ran beside dW_1; dW_0 stays
                 # after this GEMM (a fused SGD updates W_0 in place)
-                main.wait_stream(side)
+                if not (fused and self._tail_main):
+                    main.wait_stream(side)
                 sc = self._dx_scatter
                 K.gemm(cur, self.w["w0"], dx, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=G[1], beta=1.0, aux2=dx0,
                        col_groups=sc[1] if sc else (), col_group_width=sc[0] if sc else 0)
                 weight_grad("w0", cur, xs[0])
+        if fused and self._tail_main:
+            main.wait_stream(side)  # bias column sums (side stream) before the optimizer reads them
         self.grads.update(bias)
         return dx
 

@@ -312,6 +312,10 @@ def test_dcn_side_fused_matches_separate_kernels(rows, cols, nl, dt):
         assert torch.equal(sums[l], K.column_sum(gus[l]))
     ref = sum(gs[l].double() * us[l].double() for l in range(nl))
     assert (dx0.double() - ref).abs().max().item() <= 1e-6 * (ref.abs().max().item() + 1)
+    only = torch.full((rows, cols), float("nan"), device="cuda")
+    K.dcn_side_fused(gs, us, None, only, None)  # dx0 only (DMT_DCN_TAIL=main)
+    torch.cuda.synchronize()
+    assert torch.equal(only, want)
 
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
