@@ -825,7 +825,9 @@ def bucketing_gbs(torch, K, arm, rank, hbm) -> dict:
     gbs = nbytes / (ms * 1e-3) / 1e9
     return {"kernel": "dmt::kjt bucketize (step a)", "launch_ms": ms, "algorithmic_bytes": nbytes, "achieved": gbs,
             "unit": "GB/s", "peak": hbm, "frac": gbs / hbm,
-            "note": "inputs L2-resident after the first launch (the KJT is 17 MB), so frac can exceed the HBM line"}
+            "note": "inputs L2-resident after the first launch (the KJT is 17 MB), so frac can exceed the HBM line; "
+                    "timed standalone: at one rank whose slots are the features in order the training step skips "
+                    "it (the input KJT is already the bucketized KJT)"}
 
 
 def nvlink_busbw(torch, dist, dev, N) -> float:

@@ -532,6 +532,18 @@ class SpttEngine:
     def _forward_after_a(self, kjts: dict, save: bool, check_indices: bool, peer_a: bool) -> dict:
         p, fab, dev = self.plan, self.fabric, self.device
         world = list(range(p.G))
+        if (p.G == 1 and len(self.local) == 1 and self.capacity is None and self.trace is None
+                and list(p.a_slot_feature) == list(range(len(p.features)))):
+            # one rank whose slots are the features in order: the bucketized
+            # KJT is the input KJT itself (no bucketize pass, offsets reused)
+            (r,) = self.local
+            kj = kjts[r]
+            if kj.B != p.B or kj.F != len(p.features):
+                raise DomainError("KJT shape does not match the plan")
+            offs = kj.offsets if kj.offsets is not None else K.lengths_to_offsets(kj.lengths)
+            return self._forward_from_b({r: kj.lengths}, {r: kj.values},
+                                        {r: p.a_send_value_splits(kj.nnz_per_feature)}, save, check_indices,
+                                        recv_offs={r: offs})
         # step a: bucketize per src, exchange lengths then values
         send_len, send_val, len_splits, val_splits = {}, {}, {}, {}
         for r in self.local:
@@ -609,13 +621,16 @@ class SpttEngine:
         self.trace.record_device("a", r, world, counts, 4)
 
     def _forward_from_b(self, recv_len: dict, recv_val: dict, recv_val_splits: dict, save: bool,
-                        check_indices: bool) -> dict:
+                        check_indices: bool, recv_offs: Optional[dict] = None) -> dict:
         p, fab, dev = self.plan, self.fabric, self.device
         # step b: lookup (+ fused permute) on every owner
         self._owner = {}
         err = torch.zeros(1, dtype=torch.int32, device=dev) if check_indices else None
         for r in self.local:
-            offsets = K.lengths_to_offsets(recv_len[r][: p.owner_bags(r)])
+            if recv_offs is not None:
+                offsets = recv_offs[r]
+            else:
+                offsets = K.lengths_to_offsets(recv_len[r][: p.owner_bags(r)])
             nnz = sum(recv_val_splits[r])
             if self.capacity is not None:
                 # pack the capacity-padded (src, shard) regions back to back
