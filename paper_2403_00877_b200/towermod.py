@@ -166,6 +166,7 @@ class TowerModule:
     # behind the persistent GEMMs at C2: those kernels cannot co-reside)
     _side_fused = os.environ.get("DMT_DCN_SIDE", "fused") == "fused"
     _tail_main = os.environ.get("DMT_DCN_TAIL", "side") == "main"
+    _dw_concurrent = os.environ.get("DMT_DW_STREAM", "0") == "1"  # measured neutral at C2 (profiles/r2_step_ab.txt)
 
     """Device TM of one tower: forward / backward / SGD on libdmt GEMMs.
 
@@ -380,6 +381,12 @@ class TowerModule:
             weight_grad(f"w{layer}", cur, xs[layer])
         return dx
 
+    def _dw_stream(self) -> torch.cuda.Stream:
+        st = getattr(self, "_dws", None)
+        if st is None or st.device != torch.cuda.current_stream().device:
+            st = self._dws = torch.cuda.Stream(device=torch.cuda.current_stream().device, priority=-1)
+        return st
+
     def _aux_stream(self) -> torch.cuda.Stream:
         st = getattr(self, "_aux", None)
         if st is None or st.device != torch.cuda.current_stream().device:
@@ -402,6 +409,20 @@ class TowerModule:
         L_ = self.cfg.cross_layers
         dev, dt = x0.device, self.dtype
         main, side = torch.cuda.current_stream(), self._aux_stream()
+        # dW GEMMs on their own stream: dW_l (3328^2 outputs: 169 pair tiles =
+        # 2.28 persistent waves) and the next dX GEMM are independent, so the
+        # next GEMM's CTAs fill the SMs the dW's partial last wave leaves idle
+        conc = self._dw_concurrent
+        dws = self._dw_stream() if conc else None
+
+        def wgrad(name, a, b):
+            if not conc:
+                weight_grad(name, a, b)
+                return
+            dws.wait_stream(main)
+            with torch.cuda.stream(dws):
+                weight_grad(name, a, b)
+
         G = [None] + [torch.empty((rows, M), dtype=dt, device=dev) for _ in range(L_)]
         gu = [torch.empty((rows, M), dtype=dt, device=dev) for _ in range(L_)]
         dx0 = torch.empty((rows, M), dtype=torch.float32, device=dev)
@@ -442,7 +463,7 @@ class TowerModule:
 
         K.gemm(gy, self.w["w_proj"], G[L_], trans_b=True, epilogue=L.EPI_DCN_BWD, x0=x0, aux=gu[L_ - 1])
         side_work(L_ - 1)
-        weight_grad("w_proj", gy, xs[-1])
+        wgrad("w_proj", gy, xs[-1])
         dx = self._new_dx(x0)
         for layer in range(L_ - 1, -1, -1):
             cur = gu[layer]
@@ -450,7 +471,7 @@ class TowerModule:
                 K.gemm(cur, self.w[f"w{layer}"], G[layer], trans_b=True, epilogue=L.EPI_DCN_BWD, c=G[layer + 1],
                        beta=1.0, x0=x0, aux=gu[layer - 1])
                 side_work(layer - 1)
-                weight_grad(f"w{layer}", cur, xs[layer])
+                wgrad(f"w{layer}", cur, xs[layer])
             else:
                 # the side stream's last dx0 term ran beside dW_1; dW_0 stays
                 # after this GEMM (a fused SGD updates W_0 in place)
@@ -459,7 +480,9 @@ class TowerModule:
                 sc = self._dx_scatter
                 K.gemm(cur, self.w["w0"], dx, trans_b=True, epilogue=L.EPI_DCN_FINAL, c=G[1], beta=1.0, aux2=dx0,
                        col_groups=sc[1] if sc else (), col_group_width=sc[0] if sc else 0)
-                weight_grad("w0", cur, xs[0])
+                wgrad("w0", cur, xs[0])
+        if conc:
+            main.wait_stream(dws)  # weight updates / grads complete before the caller goes on
         if fused and self._tail_main:
             main.wait_stream(side)  # bias column sums (side stream) before the optimizer reads them
         self.grads.update(bias)
